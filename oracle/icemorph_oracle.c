@@ -1,0 +1,497 @@
+/* oracle/icemorph_oracle.c — TEST INFRASTRUCTURE ONLY (see icemorph_oracle.h).
+ *
+ * CPU restatement of the reference hot path, each function citing the
+ * reference file:line it follows.  Compiled with -ffp-contract=off so every
+ * + - * / sqrt rounds exactly as the reference build does.
+ */
+#define _GNU_SOURCE
+#include "icemorph_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+static __thread char g_err[1024];
+
+const char* or_last_error(void) { return g_err; }
+
+static int set_err(int code, const char* msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg);
+  return code;
+}
+
+/* vec.hpp:35-36, 56-60: s = (dx*dx + dy*dy) + dz*dz, d = sqrt(s). */
+static double norm3(double x, double y, double z) { return sqrt(x * x + y * y + z * z); }
+
+static double dist3(const double* a, const double* b) {
+  return norm3(a[0] - b[0], a[1] - b[1], a[2] - b[2]);
+}
+
+/* rbf.cpp:28-50 */
+double or_eval_wendland(int kind, double eta) {
+  if (eta >= 1.0) return 0.0;
+  const double u = 1.0 - eta;
+  switch (kind) {
+    case 0: return u * u;
+    case 1: {
+      const double u2 = u * u;
+      return u2 * u2 * (4.0 * eta + 1.0);
+    }
+    case 2: {
+      const double u2 = u * u;
+      const double u6 = u2 * u2 * u2;
+      return u6 * ((35.0 / 3.0) * eta * eta + 6.0 * eta + 1.0);
+    }
+    case 3: {
+      const double u2 = u * u;
+      const double u8 = u2 * u2 * u2 * u2;
+      return u8 * (32.0 * eta * eta * eta + 25.0 * eta * eta + 8.0 * eta + 1.0);
+    }
+  }
+  return 0.0;
+}
+
+/* rbf.cpp:52-54 */
+double or_eval_basis(int kind, double R, double distance) {
+  return or_eval_wendland(kind, distance / R);
+}
+
+/* ---- incremental Cholesky, rbf.cpp:71-121 (packed row-major lower) ---- */
+typedef struct {
+  size_t n, cap;
+  double* lower;
+  double max_diag, smallest_pivot;
+} chol_t;
+
+static int chol_init(chol_t* f, size_t cap) {
+  f->n = 0;
+  f->cap = cap;
+  f->max_diag = 0.0;
+  f->smallest_pivot = 0.0;
+  f->lower = (double*)malloc(sizeof(double) * (cap * (cap + 1) / 2 + 1));
+  return f->lower ? 0 : 3;
+}
+
+static void chol_free(chol_t* f) { free(f->lower); }
+
+/* rbf.cpp:71-100.  Returns 0, or 2 with the reference message. */
+static int chol_append(chol_t* f, const double* column) {
+  const size_t k = f->n;
+  double* row = f->lower + k * (k + 1) / 2;
+  double sq = 0.0;
+  for (size_t j = 0; j < k; ++j) {
+    const double* lj = f->lower + j * (j + 1) / 2;
+    double s = column[j];
+    for (size_t m = 0; m < j; ++m) s -= lj[m] * row[m];
+    row[j] = s / lj[j];
+    sq += row[j] * row[j];
+  }
+  const double diag = column[k];
+  if (diag > f->max_diag) f->max_diag = diag; /* std::max(max_diag_, diag) */
+  const double pivot_sq = diag - sq;
+  const double pivot = pivot_sq > 0.0 ? sqrt(pivot_sq) : 0.0;
+  if (!(pivot > 1e-14 * f->max_diag)) {
+    snprintf(g_err, sizeof g_err,
+             "matrix not numerically positive definite at row %zu (pivot %f)", k, pivot);
+    return 2;
+  }
+  row[k] = pivot;
+  if (f->n == 0 || pivot < f->smallest_pivot) f->smallest_pivot = pivot;
+  ++f->n;
+  return 0;
+}
+
+/* rbf.cpp:102-121 */
+static void chol_solve(const chol_t* f, const double* rhs, double* x) {
+  const size_t n = f->n;
+  for (size_t i = 0; i < n; ++i) {
+    const double* li = f->lower + i * (i + 1) / 2;
+    double s = rhs[i];
+    for (size_t j = 0; j < i; ++j) s -= li[j] * x[j];
+    x[i] = s / li[i];
+  }
+  for (size_t i = n; i-- > 0;) {
+    double s = x[i];
+    for (size_t j = i + 1; j < n; ++j) s -= f->lower[j * (j + 1) / 2 + i] * x[j];
+    x[i] = s / f->lower[i * (i + 1) / 2 + i];
+  }
+}
+
+/* rbf.cpp:125-140 */
+static int rethrow_conditioning(const double* pts, size_t failed) {
+  size_t nearest = 0;
+  double best = INFINITY;
+  for (size_t i = 0; i < failed; ++i) {
+    const double d = dist3(pts + 3 * i, pts + 3 * failed);
+    if (d < best) {
+      best = d;
+      nearest = i;
+    }
+  }
+  snprintf(g_err, sizeof g_err,
+           "ill-conditioned control set: points %zu and %zu are too close (distance %f)",
+           nearest, failed, best);
+  return 2;
+}
+
+/* rbf.cpp:144-193 */
+int or_solve_weights(const double* pts, const double* disp, size_t n, int kind,
+                     double R, double* alpha_out) {
+  memset(alpha_out, 0, sizeof(double) * 3 * n);
+  if (n == 0) return 0;
+  int all_zero = 1;
+  for (size_t i = 0; i < 3 * n; ++i)
+    if (disp[i] != 0.0) {
+      all_zero = 0;
+      break;
+    }
+  if (all_zero) return 0;
+  chol_t f;
+  if (chol_init(&f, n)) return set_err(3, "out of memory");
+  double* column = (double*)malloc(sizeof(double) * (n + 1));
+  double* rhs = (double*)malloc(sizeof(double) * n);
+  double* sol = (double*)malloc(sizeof(double) * n);
+  int rc = 0;
+  for (size_t k = 0; k < n && rc == 0; ++k) {
+    for (size_t j = 0; j < k; ++j)
+      column[j] = or_eval_basis(kind, R, dist3(pts + 3 * j, pts + 3 * k));
+    column[k] = 1.0;
+    if (chol_append(&f, column)) rc = rethrow_conditioning(pts, k);
+  }
+  if (rc == 0) {
+    for (int axis = 0; axis < 3; ++axis) {
+      for (size_t i = 0; i < n; ++i) rhs[i] = disp[3 * i + axis];
+      chol_solve(&f, rhs, sol);
+      for (size_t i = 0; i < n; ++i) alpha_out[3 * i + axis] = sol[i];
+    }
+  }
+  free(column);
+  free(rhs);
+  free(sol);
+  chol_free(&f);
+  return rc;
+}
+
+/* rbf.cpp:195-203 */
+static void interp1(const double* ctrl, const double* alpha, size_t nc, int kind, double R,
+                    const double* q, double* out) {
+  double rx = 0.0, ry = 0.0, rz = 0.0;
+  for (size_t i = 0; i < nc; ++i) {
+    const double phi = or_eval_basis(kind, R, dist3(ctrl + 3 * i, q));
+    if (phi != 0.0) {
+      rx += alpha[3 * i] * phi;
+      ry += alpha[3 * i + 1] * phi;
+      rz += alpha[3 * i + 2] * phi;
+    }
+  }
+  out[0] = rx;
+  out[1] = ry;
+  out[2] = rz;
+}
+
+int or_eval_interpolant(const double* ctrl, const double* alpha, size_t nc, int kind,
+                        double R, const double* q, size_t nq, double* out) {
+  for (size_t i = 0; i < nq; ++i) interp1(ctrl, alpha, nc, kind, R, q + 3 * i, out + 3 * i);
+  return 0;
+}
+
+/* greedy.cpp:20-33 */
+static int check_config(double tol, size_t max_levels, size_t cap, double R) {
+  if (!(tol > 0.0 && tol < 1.0)) return set_err(1, "greedy tolerance must lie in (0,1)");
+  if (max_levels < 1) return set_err(1, "at least one level is required");
+  if (cap < 1) return set_err(1, "per-level point cap must be positive");
+  if (!(R > 0.0)) return set_err(1, "basis support radius must be positive");
+  return 0;
+}
+
+/* greedy.cpp:35-39 */
+static double max_magnitude(const double* v, size_t n) {
+  double m = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    const double x = norm3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+    m = (m < x) ? x : m; /* std::max(m, x) */
+  }
+  return m;
+}
+
+/* greedy.cpp:41-56 */
+static int rethrow_conditioning_nodes(const double* pos, const size_t* controls, size_t nc,
+                                      size_t failed) {
+  size_t nearest = failed;
+  double best = INFINITY;
+  for (size_t m = 0; m < nc; ++m) {
+    const double d = dist3(pos + 3 * controls[m], pos + 3 * failed);
+    if (d < best) {
+      best = d;
+      nearest = controls[m];
+    }
+  }
+  snprintf(g_err, sizeof g_err,
+           "ill-conditioned control set: surface nodes %zu and %zu are too close "
+           "(distance %f)",
+           nearest, failed, best);
+  return 2;
+}
+
+/* greedy.cpp:60-170 */
+int or_greedy_level(const double* pos, const double* target, size_t n, double tol,
+                    size_t cap_cfg, int kind, double R, size_t level_index,
+                    size_t* out_idx, double* out_alpha, size_t* out_nc,
+                    double* out_achieved, int* out_cap_hit, double* out_target_max,
+                    size_t* out_rec_points, double* out_rec_error, size_t* out_nrec,
+                    double* out_residual) {
+  (void)level_index;
+  int rc = check_config(tol, 1, cap_cfg, R);
+  if (rc) return rc;
+  if (n == 0) return set_err(1, "surface point set is empty");
+  for (size_t i = 0; i < 3 * n; ++i)
+    if (!isfinite(target[i])) return set_err(1, "target displacement is not finite");
+
+  const double target_max = max_magnitude(target, n);
+  const size_t cap = cap_cfg < n ? cap_cfg : n;
+  size_t nc = 0, nrec = 0;
+  size_t* controls = out_idx;
+  char* selected = (char*)calloc(n, 1);
+  double* alpha = out_alpha;
+  double* column = (double*)malloc(sizeof(double) * (cap + 1));
+  double* rhs = (double*)malloc(sizeof(double) * cap);
+  double* sol = (double*)malloc(sizeof(double) * cap);
+  double* residual = out_residual ? out_residual : (double*)malloc(sizeof(double) * 3 * n);
+  chol_t f;
+  if (chol_init(&f, cap)) return set_err(3, "out of memory");
+
+  size_t node = 0; /* greedy.cpp:115 — seed with the first surface node */
+  double achieved = 0.0;
+  int cap_hit = 0;
+  for (;;) {
+    /* insert_control(node), greedy.cpp:86-112 */
+    for (size_t m = 0; m < nc; ++m)
+      column[m] = or_eval_basis(kind, R, dist3(pos + 3 * controls[m], pos + 3 * node));
+    column[nc] = 1.0;
+    if (chol_append(&f, column)) {
+      rc = rethrow_conditioning_nodes(pos, controls, nc, node);
+      break;
+    }
+    controls[nc++] = node;
+    selected[node] = 1;
+    for (int axis = 0; axis < 3; ++axis) {
+      for (size_t m = 0; m < nc; ++m) rhs[m] = target[3 * controls[m] + axis];
+      chol_solve(&f, rhs, sol);
+      for (size_t m = 0; m < nc; ++m) alpha[3 * m + axis] = sol[m];
+    }
+
+    /* sweep, greedy.cpp:122-143 */
+    double max_norm = -1.0;
+    size_t argmax = n;
+    for (size_t i = 0; i < n; ++i) {
+      double fx = 0.0, fy = 0.0, fz = 0.0;
+      for (size_t m = 0; m < nc; ++m) {
+        const double phi = or_eval_basis(kind, R, dist3(pos + 3 * i, pos + 3 * controls[m]));
+        if (phi != 0.0) {
+          fx += alpha[3 * m] * phi;
+          fy += alpha[3 * m + 1] * phi;
+          fz += alpha[3 * m + 2] * phi;
+        }
+      }
+      residual[3 * i] = target[3 * i] - fx;
+      residual[3 * i + 1] = target[3 * i + 1] - fy;
+      residual[3 * i + 2] = target[3 * i + 2] - fz;
+      const double nrm = norm3(residual[3 * i], residual[3 * i + 1], residual[3 * i + 2]);
+      if (!selected[i] && nrm > max_norm) {
+        max_norm = nrm;
+        argmax = i;
+      }
+    }
+    double overall = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      const double e = norm3(residual[3 * i], residual[3 * i + 1], residual[3 * i + 2]);
+      overall = (overall < e) ? e : overall; /* std::max */
+    }
+    achieved = target_max > 0.0 ? overall / target_max : 0.0;
+    if (out_rec_points) out_rec_points[nrec] = nc;
+    if (out_rec_error) out_rec_error[nrec] = achieved;
+    ++nrec;
+    /* greedy.cpp:146-152 */
+    if (achieved < tol) break;
+    if (nc >= cap || argmax == n) {
+      cap_hit = 1;
+      break;
+    }
+    node = argmax;
+  }
+  *out_nc = nc;
+  *out_achieved = achieved;
+  *out_cap_hit = cap_hit;
+  *out_target_max = target_max;
+  if (out_nrec) *out_nrec = nrec;
+  if (!out_residual) free(residual);
+  free(selected);
+  free(column);
+  free(rhs);
+  free(sol);
+  chol_free(&f);
+  return rc;
+}
+
+/* greedy.cpp:172-195 */
+int or_run_multilevel(const double* pos, const double* target, size_t n, double tol,
+                      size_t max_levels, size_t cap, int kind, double R,
+                      size_t* out_nlevels, size_t* out_nc, size_t* out_idx,
+                      double* out_alpha, double* out_achieved, int* out_cap_hit,
+                      double* out_level_target_max, size_t* out_nrec,
+                      double* out_rec_error, double* out_target_max,
+                      double* out_final_residual) {
+  int rc = check_config(tol, max_levels, cap, R);
+  if (rc) return rc;
+  const double target_max = max_magnitude(target, n);
+  *out_target_max = target_max;
+  const size_t stride = cap < n ? cap : n;
+  double* current = (double*)malloc(sizeof(double) * 3 * (n ? n : 1));
+  double* next = (double*)malloc(sizeof(double) * 3 * (n ? n : 1));
+  memcpy(current, target, sizeof(double) * 3 * n);
+  const double entry_threshold = pow(tol, (double)max_levels) * target_max;
+  size_t nl = 0;
+  for (size_t l = 0; l < max_levels; ++l) {
+    const double current_max = max_magnitude(current, n);
+    if (l > 0 && (current_max == 0.0 || current_max < entry_threshold)) break;
+    rc = or_greedy_level(pos, current, n, tol, cap, kind, R, l, out_idx + l * stride,
+                         out_alpha + 3 * l * stride, out_nc + l, out_achieved + l,
+                         out_cap_hit + l, out_level_target_max + l, NULL,
+                         out_rec_error ? out_rec_error + l * stride : NULL, out_nrec + l,
+                         next);
+    if (rc) break;
+    double* t = current;
+    current = next;
+    next = t;
+    ++nl;
+  }
+  *out_nlevels = nl;
+  if (rc == 0 && out_final_residual) memcpy(out_final_residual, current, sizeof(double) * 3 * n);
+  free(current);
+  free(next);
+  return rc;
+}
+
+/* ---- wall distance, wall_distance.cpp:13-31 ---- */
+typedef struct {
+  const double* nodes;
+  size_t lo, hi;
+  const double* surf;
+  size_t ns;
+  double* out;
+} nn_job;
+
+static void* nn_work(void* p) {
+  nn_job* j = (nn_job*)p;
+  for (size_t i = j->lo; i < j->hi; ++i) {
+    const double* q = j->nodes + 3 * i;
+    double best = INFINITY;
+    for (size_t s = 0; s < j->ns; ++s) {
+      const double* a = j->surf + 3 * s;
+      const double dx = a[0] - q[0], dy = a[1] - q[1], dz = a[2] - q[2];
+      const double d2 = dx * dx + dy * dy + dz * dz; /* squared_distance, vec.hpp:59 */
+      if (d2 < best) best = d2;
+    }
+    j->out[i] = sqrt(best); /* kdtree.cpp:79 */
+  }
+  return NULL;
+}
+
+int or_build_distance_index(const double* nodes, size_t n_nodes, int dim,
+                            const size_t* surface, size_t n_surface, double* out_dist,
+                            int nthreads) {
+  if (n_surface == 0)
+    return set_err(1, "cannot build a distance index for an empty patch");
+  if (dim != 2 && dim != 3) return set_err(1, "kd-tree dim must be 2 or 3");
+  double* surf = (double*)malloc(sizeof(double) * 3 * n_surface);
+  for (size_t s = 0; s < n_surface; ++s) memcpy(surf + 3 * s, nodes + 3 * surface[s], 24);
+  if (nthreads < 1) nthreads = 1;
+  pthread_t th[256];
+  nn_job jobs[256];
+  if (nthreads > 256) nthreads = 256;
+  for (int t = 0; t < nthreads; ++t) {
+    jobs[t] = (nn_job){nodes, n_nodes * t / nthreads, n_nodes * (t + 1) / nthreads, surf,
+                       n_surface, out_dist};
+    if (nthreads > 1)
+      pthread_create(&th[t], NULL, nn_work, &jobs[t]);
+    else
+      nn_work(&jobs[t]);
+  }
+  if (nthreads > 1)
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  for (size_t s = 0; s < n_surface; ++s) out_dist[surface[s]] = 0.0; /* :29 */
+  free(surf);
+  return 0;
+}
+
+/* wall_distance.cpp:40-44; psi_kind 1 swaps in eval_wendland(C2, xi). */
+double or_eval_wall_function(int psi_kind, double D, double d) {
+  if (D <= 0.0) return d == 0.0 ? 1.0 : 0.0;
+  const double xi = d / D;
+  if (psi_kind == 1) return or_eval_wendland(1, xi);
+  return xi < 1.0 ? 1.0 - xi : 0.0;
+}
+
+/* wall_distance.cpp:46-64 */
+typedef struct {
+  const double *nodes, *dist, *ctrl, *alpha;
+  size_t nc, lo, hi;
+  double D, R;
+  int psi_kind, kind;
+  size_t* idx;
+  double* val;
+  size_t count;
+} vu_job;
+
+static void* vu_work(void* p) {
+  vu_job* j = (vu_job*)p;
+  size_t k = 0;
+  for (size_t i = j->lo; i < j->hi; ++i) {
+    const double d = j->dist[i];
+    if (d >= j->D) continue;
+    const double psi = or_eval_wall_function(j->psi_kind, j->D, d);
+    double v[3];
+    interp1(j->ctrl, j->alpha, j->nc, j->kind, j->R, j->nodes + 3 * i, v);
+    j->idx[k] = i;
+    j->val[3 * k] = v[0] * psi;
+    j->val[3 * k + 1] = v[1] * psi;
+    j->val[3 * k + 2] = v[2] * psi;
+    ++k;
+  }
+  j->count = k;
+  return NULL;
+}
+
+int or_update_volume(const double* nodes, size_t n_nodes, const double* dist,
+                     const double* ctrl, const double* alpha, size_t nc, double D,
+                     int psi_kind, int kind, double R, size_t* out_idx, double* out_val,
+                     size_t* out_n, int nthreads) {
+  *out_n = 0;
+  if (D <= 0.0) return 0; /* wall_distance.cpp:54 */
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  pthread_t th[256];
+  vu_job jobs[256];
+  for (int t = 0; t < nthreads; ++t) {
+    const size_t lo = n_nodes * t / nthreads, hi = n_nodes * (t + 1) / nthreads;
+    jobs[t] = (vu_job){nodes, dist, ctrl, alpha, nc, lo, hi, D, R, psi_kind, kind,
+                       out_idx + lo, out_val + 3 * lo, 0};
+    if (nthreads > 1)
+      pthread_create(&th[t], NULL, vu_work, &jobs[t]);
+    else
+      vu_work(&jobs[t]);
+  }
+  if (nthreads > 1)
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  /* compact the per-slice outputs in slice (= ascending node) order */
+  size_t k = 0;
+  for (int t = 0; t < nthreads; ++t) {
+    memmove(out_idx + k, jobs[t].idx, sizeof(size_t) * jobs[t].count);
+    memmove(out_val + 3 * k, jobs[t].val, sizeof(double) * 3 * jobs[t].count);
+    k += jobs[t].count;
+  }
+  *out_n = k;
+  return 0;
+}
