@@ -1,0 +1,205 @@
+/* include/icemorph_b200.h — C-ABI of the B200-native RBF mesh-deformation
+ * hot path (arXiv 2107.13887, reference "icemorph").
+ *
+ * This is the drop-in boundary: plain pointers, sizes and POD structs, no
+ * C++ or torch types.  Every entry point replaces one function of the
+ * reference's public C++ API (proj/include/icemorph/*.hpp) and states which.
+ * Vectors are AoS x,y,z triples of doubles (the reference's Vec3 layout,
+ * vec.hpp:8-12); node indices are size_t.
+ *
+ * Errors: C++ exceptions cannot cross a C ABI, so every call returns a
+ * status and leaves the reference's exception text in im_last_error(ctx):
+ *   IM_OK                0
+ *   IM_INVALID_ARGUMENT  1   std::invalid_argument in the reference
+ *   IM_SOLVE_ERROR       2   icemorph::SolveError (rbf.hpp:13-16)
+ *   IM_RUNTIME_ERROR     3   CUDA / other runtime failures
+ * The C++ shim (paper_2107_13887_b200/cpp) rethrows the same types.
+ *
+ * Threading: a context owns one CUDA stream and its scratch; calls on
+ * different contexts may run concurrently (the reference's reentrancy,
+ * SPEC.md:350).  A context must not be used by two threads at once.
+ *
+ * Precision (additive extension):
+ *   IM_EXACT   reference arithmetic order, bit-identical results
+ *   IM_FP64    FMA fast path, <= 1e-10 relative to the reference (default
+ *              for the volume update)
+ */
+#ifndef ICEMORPH_B200_H
+#define ICEMORPH_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IM_OK 0
+#define IM_INVALID_ARGUMENT 1
+#define IM_SOLVE_ERROR 2
+#define IM_RUNTIME_ERROR 3
+
+/* WendlandKind, rbf.hpp:18 */
+#define IM_C0 0
+#define IM_C2 1
+#define IM_C4 2
+#define IM_C6 3
+
+/* taper kind (additive): reference linear psi (wall_distance.cpp:40-44) or
+ * Wendland C2 of xi (BASELINE cfg1) */
+#define IM_PSI_LINEAR 0
+#define IM_PSI_WENDLAND_C2 1
+
+#define IM_EXACT 0
+#define IM_FP64 1
+
+typedef struct im_context im_context;
+
+/* BasisFunction, rbf.hpp:25-28 */
+typedef struct {
+  int kind;
+  double support_radius;
+} im_basis;
+
+/* GreedyConfig, greedy.hpp:12-17 */
+typedef struct {
+  double tolerance;
+  size_t max_levels;
+  size_t max_points_per_level;
+  im_basis basis;
+} im_greedy_config;
+
+/* WallFunction, wall_distance.hpp:26-29, plus the taper kind */
+typedef struct {
+  double reduction_factor;
+  double support_distance;
+  int psi_kind;
+} im_wall_function;
+
+/* ---- context ------------------------------------------------------------ */
+int im_context_create(im_context** out, int device);
+int im_context_destroy(im_context* ctx);
+const char* im_last_error(const im_context* ctx);
+/* device time of the last hot-path kernel sequence, milliseconds */
+double im_last_device_ms(const im_context* ctx);
+/* library build tag (sm_100a) */
+const char* im_version(void);
+
+/* ---- host scalar helpers (no device work) --------------------------------
+ * eval_wendland  rbf.hpp:30 / rbf.cpp:28-50
+ * eval_basis     rbf.hpp:31 / rbf.cpp:52-54
+ * make_wall_function / eval_wall_function  wall_distance.hpp:31-32 */
+double im_eval_wendland(int kind, double eta);
+double im_eval_basis(im_basis basis, double distance);
+int im_make_wall_function(double reduction_factor, double level_target_max,
+                          im_wall_function* out);
+double im_eval_wall_function(const im_wall_function* wf, double wall_distance);
+
+/* ---- rbf ------------------------------------------------------------------
+ * solve_weights, rbf.hpp:74-76 (rbf.cpp:144-193).  alpha_out: 3n doubles. */
+int im_solve_weights(im_context* ctx, const double* points, const double* displacements,
+                     size_t n, im_basis basis, double* alpha_out);
+
+/* eval_interpolant, rbf.hpp:80-81 (rbf.cpp:195-203), batched over n_query
+ * queries.  out: 3 n_query doubles. */
+int im_eval_interpolant(im_context* ctx, const double* control_positions, const double* alpha,
+                        size_t n_control, im_basis basis, const double* queries,
+                        size_t n_query, int precision, double* out);
+
+/* ---- greedy -----------------------------------------------------------------
+ * greedy_level, greedy.hpp:51-54 (greedy.cpp:60-170).  Always exact.
+ * Let m = min(max_points_per_level, n).  Caller buffers:
+ *   control_indices[m], alpha[3m], record_points[m], record_error[m],
+ *   record_seconds[m] (may be NULL), residual[3n] (may be NULL). */
+int im_greedy_level(im_context* ctx, const double* surface_positions, const double* target,
+                    size_t n, const im_greedy_config* config, size_t level_index,
+                    size_t* control_indices, double* alpha, size_t* n_controls,
+                    double* achieved_error, int* cap_hit, double* target_max,
+                    double* elapsed_seconds, size_t* record_points, double* record_error,
+                    double* record_seconds, size_t* n_records, double* residual);
+
+/* run_multilevel, greedy.hpp:66-68 (greedy.cpp:172-195).  Level l's arrays
+ * start at offset l*m (m as above); per-level scalars have max_levels slots. */
+int im_run_multilevel(im_context* ctx, const double* surface_positions, const double* target,
+                      size_t n, const im_greedy_config* config, size_t* n_levels,
+                      size_t* n_controls, size_t* control_indices, double* alpha,
+                      double* achieved_error, int* cap_hit, double* level_target_max,
+                      double* elapsed_seconds, size_t* n_records, double* record_error,
+                      double* target_max, double* final_residual);
+
+/* ---- wall distance / volume reduction -----------------------------------------
+ * build_distance_index, wall_distance.hpp:20-22 (wall_distance.cpp:13-31).
+ * nodes: 3 n_nodes doubles; distances_out: n_nodes doubles. */
+int im_build_distance_index(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
+                            const size_t* surface_nodes, size_t n_surface,
+                            double* distances_out);
+
+/* update_volume, wall_distance.hpp:40-42 (wall_distance.cpp:46-64).
+ * entry_nodes[n_nodes] / entry_values[3 n_nodes] receive the ascending
+ * sparse update; *n_entries its length. */
+int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes,
+                     const double* distances, const double* control_positions,
+                     const double* alpha, size_t n_control, const im_wall_function* wf,
+                     im_basis basis, int precision, size_t* entry_nodes,
+                     double* entry_values, size_t* n_entries);
+
+/* ---- pipeline -----------------------------------------------------------------
+ * deform, pipeline.hpp:54-56 (pipeline.cpp:19-106) on a mesh given as its
+ * node array and the node lists of the deforming patch and of the pinned
+ * markers (the hot path reads nothing else of Mesh).
+ * displacement: 3 n_patch doubles, one per patch node (DisplacementField::at).
+ * support_distance < 0 selects the reference D_l = volume_k * target_max_l
+ * (pipeline.cpp:66); >= 0 (inf allowed) is an absolute D (additive).
+ * deformed_nodes: 3 n_nodes doubles.  Per-level outputs have max_levels
+ * slots; quality metrics are out of scope (compute_quality = false). */
+typedef struct {
+  im_greedy_config greedy;
+  double volume_k;
+  double support_distance;
+  int psi_kind;
+  int precision;
+} im_deform_config;
+
+typedef struct {
+  size_t n_levels;
+  double target_max;
+  double surface_max_error;
+  double surface_mean_error;
+  double total_seconds;
+  double greedy_seconds;
+  double distance_seconds;
+  double volume_seconds;
+} im_deform_report;
+
+int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
+              const size_t* patch_nodes, size_t n_patch, const double* displacement,
+              const size_t* pinned_nodes, size_t n_pinned, const im_deform_config* config,
+              double* deformed_nodes, im_deform_report* report, size_t* level_points,
+              double* level_achieved, int* level_cap_hit, double* level_support_distance,
+              size_t* level_touched, double* level_seconds);
+
+/* ---- resident plans (inputs kept in HBM between calls) ------------------------
+ * A volume plan uploads the mesh nodes once and computes the wall distances
+ * on the device; im_volume_plan_run then performs the culling + compaction
+ * + volume update for one level entirely on the device and accumulates the
+ * update into the plan's resident displacement field.  cutoff: +inf for exact
+ * distances at every node, a finite value to cull beyond it (nodes farther
+ * get +inf), < 0 to skip the distance pass (D = inf workloads, psi == 1). */
+typedef struct im_volume_plan im_volume_plan;
+int im_volume_plan_create(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
+                          const size_t* surface_nodes, size_t n_surface, double cutoff,
+                          im_volume_plan** out);
+int im_volume_plan_destroy(im_volume_plan* plan);
+int im_volume_plan_set_controls(im_volume_plan* plan, const double* control_positions,
+                                const double* alpha, size_t n_control);
+/* one level: compaction at D + update over the active set, accumulated into
+ * the resident field; returns the active count; device ms in *device_ms */
+int im_volume_plan_run(im_volume_plan* plan, const im_wall_function* wf, im_basis basis,
+                       int precision, size_t* n_active, double* device_ms);
+int im_volume_plan_reset_field(im_volume_plan* plan);
+int im_volume_plan_download_field(im_volume_plan* plan, double* out_xyz);
+int im_volume_plan_distances(im_volume_plan* plan, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ICEMORPH_B200_H */

@@ -1,0 +1,402 @@
+"""ctypes binding of the C-ABI in include/icemorph_b200.h.
+
+This is the thin Python door onto the CUDA library built in-tree at
+``paper_2107_13887_b200/libicemorph_b200.so``.  There is no fallback: if the
+library is missing, or the device is not an sm_100 GPU, every call raises.
+Errors carry the reference's exception text and map onto the reference's
+exception types as pybind11 would raise them (``ValueError`` for
+std::invalid_argument, ``SolveError`` (a RuntimeError) for
+icemorph::SolveError).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libicemorph_b200.so")
+KINDS = {"c0": 0, "c2": 1, "c4": 2, "c6": 3}
+PSI = {"linear": 0, "c2": 1, "wendland_c2": 1}
+EXACT, FP64 = 0, 1
+
+_sz = C.c_size_t
+_d = C.c_double
+_pd = C.POINTER(C.c_double)
+_psz = C.POINTER(C.c_size_t)
+_pi = C.POINTER(C.c_int)
+
+
+class SolveError(RuntimeError):
+    """icemorph::SolveError (rbf.hpp:13-16)."""
+
+
+class IcemorphRuntimeError(RuntimeError):
+    pass
+
+
+class Basis(C.Structure):
+    _fields_ = [("kind", C.c_int), ("support_radius", C.c_double)]
+
+
+class GreedyConfigC(C.Structure):
+    _fields_ = [("tolerance", C.c_double), ("max_levels", C.c_size_t),
+                ("max_points_per_level", C.c_size_t), ("basis", Basis)]
+
+
+class WallFunctionC(C.Structure):
+    _fields_ = [("reduction_factor", C.c_double), ("support_distance", C.c_double),
+                ("psi_kind", C.c_int)]
+
+
+class DeformConfigC(C.Structure):
+    _fields_ = [("greedy", GreedyConfigC), ("volume_k", C.c_double),
+                ("support_distance", C.c_double), ("psi_kind", C.c_int), ("precision", C.c_int)]
+
+
+class DeformReportC(C.Structure):
+    _fields_ = [("n_levels", C.c_size_t), ("target_max", C.c_double),
+                ("surface_max_error", C.c_double), ("surface_mean_error", C.c_double),
+                ("total_seconds", C.c_double), ("greedy_seconds", C.c_double),
+                ("distance_seconds", C.c_double), ("volume_seconds", C.c_double)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library() -> C.CDLL:
+    """Load libicemorph_b200.so (raises if it was not built)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise IcemorphRuntimeError(
+                    f"{LIB_PATH} is missing: build it with __graft_entry__.build() or "
+                    "`make -C paper_2107_13887_b200`")
+            lib = C.CDLL(LIB_PATH)
+            _declare(lib)
+            _lib = lib
+    return _lib
+
+
+EXPORTS = [
+    "im_context_create", "im_context_destroy", "im_last_error", "im_last_device_ms",
+    "im_version", "im_eval_wendland", "im_eval_basis", "im_make_wall_function",
+    "im_eval_wall_function", "im_solve_weights", "im_eval_interpolant", "im_greedy_level",
+    "im_run_multilevel", "im_build_distance_index", "im_update_volume", "im_deform",
+    "im_volume_plan_create", "im_volume_plan_destroy", "im_volume_plan_set_controls",
+    "im_volume_plan_run", "im_volume_plan_reset_field", "im_volume_plan_download_field",
+    "im_volume_plan_distances",
+]
+
+
+def _declare(L):
+    L.im_context_create.argtypes = [C.POINTER(C.c_void_p), C.c_int]
+    L.im_context_destroy.argtypes = [C.c_void_p]
+    L.im_last_error.argtypes = [C.c_void_p]
+    L.im_last_error.restype = C.c_char_p
+    L.im_last_device_ms.argtypes = [C.c_void_p]
+    L.im_last_device_ms.restype = C.c_double
+    L.im_version.restype = C.c_char_p
+    L.im_eval_wendland.argtypes = [C.c_int, _d]
+    L.im_eval_wendland.restype = _d
+    L.im_eval_basis.argtypes = [Basis, _d]
+    L.im_eval_basis.restype = _d
+    L.im_make_wall_function.argtypes = [_d, _d, C.POINTER(WallFunctionC)]
+    L.im_eval_wall_function.argtypes = [C.POINTER(WallFunctionC), _d]
+    L.im_eval_wall_function.restype = _d
+    L.im_solve_weights.argtypes = [C.c_void_p, _pd, _pd, _sz, Basis, _pd]
+    L.im_eval_interpolant.argtypes = [C.c_void_p, _pd, _pd, _sz, Basis, _pd, _sz, C.c_int, _pd]
+    L.im_greedy_level.argtypes = [C.c_void_p, _pd, _pd, _sz, C.POINTER(GreedyConfigC), _sz,
+                                  _psz, _pd, _psz, _pd, _pi, _pd, _pd, _psz, _pd, _pd, _psz, _pd]
+    L.im_run_multilevel.argtypes = [C.c_void_p, _pd, _pd, _sz, C.POINTER(GreedyConfigC), _psz,
+                                    _psz, _psz, _pd, _pd, _pi, _pd, _pd, _psz, _pd, _pd, _pd]
+    L.im_build_distance_index.argtypes = [C.c_void_p, _pd, _sz, C.c_int, _psz, _sz, _pd]
+    L.im_update_volume.argtypes = [C.c_void_p, _pd, _sz, _pd, _pd, _pd, _sz,
+                                   C.POINTER(WallFunctionC), Basis, C.c_int, _psz, _pd, _psz]
+    L.im_deform.argtypes = [C.c_void_p, _pd, _sz, C.c_int, _psz, _sz, _pd, _psz, _sz,
+                            C.POINTER(DeformConfigC), _pd, C.POINTER(DeformReportC), _psz, _pd,
+                            _pi, _pd, _psz, _pd]
+    L.im_volume_plan_create.argtypes = [C.c_void_p, _pd, _sz, C.c_int, _psz, _sz, _d,
+                                        C.POINTER(C.c_void_p)]
+    L.im_volume_plan_destroy.argtypes = [C.c_void_p]
+    L.im_volume_plan_set_controls.argtypes = [C.c_void_p, _pd, _pd, _sz]
+    L.im_volume_plan_run.argtypes = [C.c_void_p, C.POINTER(WallFunctionC), Basis, C.c_int, _psz,
+                                     _pd]
+    L.im_volume_plan_reset_field.argtypes = [C.c_void_p]
+    L.im_volume_plan_download_field.argtypes = [C.c_void_p, _pd]
+    L.im_volume_plan_distances.argtypes = [C.c_void_p, _pd]
+
+
+def _dp(a):
+    return None if a is None else a.ctypes.data_as(_pd)
+
+
+def _szp(a):
+    return None if a is None else a.ctypes.data_as(_psz)
+
+
+def xyz(a) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if a.ndim == 1:
+        a = a.reshape(-1, 3)
+    if a.ndim != 2 or a.shape[1] != 3:
+        raise ValueError("expected an (n, 3) array of points")
+    return a
+
+
+def basis(kind="c2", R=1.0) -> Basis:
+    k = KINDS[kind.lower()] if isinstance(kind, str) else int(kind)
+    return Basis(k, float(R))
+
+
+@dataclass
+class LevelResult:
+    control_indices: np.ndarray
+    alpha: np.ndarray
+    achieved_error: float
+    cap_hit: bool
+    target_max: float
+    elapsed_seconds: float
+    record_points: np.ndarray
+    record_error: np.ndarray
+    record_seconds: np.ndarray | None
+    residual: np.ndarray | None
+
+
+@dataclass
+class MultilevelResult:
+    levels: list = field(default_factory=list)
+    target_max: float = 0.0
+    final_residual: np.ndarray | None = None
+
+
+class Context:
+    """One CUDA stream + scratch on one device (im_context)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = C.c_void_p()
+        rc = self.lib.im_context_create(C.byref(h), device)
+        self.h = h
+        if rc != 0:
+            msg = self.lib.im_last_error(h).decode() if h else "context creation failed"
+            self.close()
+            raise IcemorphRuntimeError(msg)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.im_context_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, rc: int):
+        if rc == 0:
+            return
+        msg = self.lib.im_last_error(self.h).decode()
+        if rc == 1:
+            raise ValueError(msg)
+        if rc == 2:
+            raise SolveError(msg)
+        raise IcemorphRuntimeError(msg)
+
+    @property
+    def last_device_ms(self) -> float:
+        return self.lib.im_last_device_ms(self.h)
+
+    # -- rbf ---------------------------------------------------------------
+    def solve_weights(self, points, displacements, kind="c2", R=1.0) -> np.ndarray:
+        p, d = xyz(points), xyz(displacements)
+        if len(p) != len(d):
+            raise ValueError("point and displacement counts differ")
+        out = np.zeros_like(p)
+        self._check(self.lib.im_solve_weights(self.h, _dp(p), _dp(d), len(p), basis(kind, R),
+                                              _dp(out)))
+        return out
+
+    def eval_interpolant(self, ctrl, alpha, kind, R, queries, precision=EXACT) -> np.ndarray:
+        c, a, q = xyz(ctrl), xyz(alpha), xyz(queries)
+        out = np.zeros_like(q)
+        self._check(self.lib.im_eval_interpolant(self.h, _dp(c), _dp(a), len(c), basis(kind, R),
+                                                 _dp(q), len(q), precision, _dp(out)))
+        return out
+
+    # -- greedy --------------------------------------------------------------
+    def greedy_level(self, pos, target, tol, cap=5000, kind="c2", R=1.0, level_index=0,
+                     max_levels=1) -> LevelResult:
+        pos, tgt = xyz(pos), xyz(target)
+        n = len(pos)
+        if len(tgt) != n:
+            raise ValueError("target size does not match surface size")
+        m = max(1, min(cap, n))
+        cfg = GreedyConfigC(tol, max_levels, cap, basis(kind, R))
+        idx = np.zeros(m, np.uint64)
+        alpha = np.zeros((m, 3))
+        rp = np.zeros(m, np.uint64)
+        re = np.zeros(m)
+        rs = np.zeros(m)
+        res = np.zeros_like(pos)
+        nc, nrec = _sz(), _sz()
+        ach, tmax, el = _d(), _d(), _d()
+        caph = C.c_int()
+        self._check(self.lib.im_greedy_level(
+            self.h, _dp(pos), _dp(tgt), n, C.byref(cfg), level_index, _szp(idx), _dp(alpha),
+            C.byref(nc), C.byref(ach), C.byref(caph), C.byref(tmax), C.byref(el), _szp(rp),
+            _dp(re), _dp(rs), C.byref(nrec), _dp(res)))
+        k, r = nc.value, nrec.value
+        return LevelResult(idx[:k].astype(np.int64), alpha[:k].copy(), ach.value,
+                           bool(caph.value), tmax.value, el.value, rp[:r].astype(np.int64),
+                           re[:r].copy(), rs[:r].copy(), res)
+
+    def run_multilevel(self, pos, target, tol, max_levels=5, cap=5000, kind="c2",
+                       R=1.0) -> MultilevelResult:
+        pos, tgt = xyz(pos), xyz(target)
+        n = len(pos)
+        m = max(1, min(cap, n))
+        L = max_levels
+        cfg = GreedyConfigC(tol, max_levels, cap, basis(kind, R))
+        nl = _sz()
+        nc = np.zeros(L, np.uint64)
+        idx = np.zeros(L * m, np.uint64)
+        alpha = np.zeros((L * m, 3))
+        ach = np.zeros(L)
+        caph = np.zeros(L, np.int32)
+        ltm = np.zeros(L)
+        el = np.zeros(L)
+        nrec = np.zeros(L, np.uint64)
+        rerr = np.zeros(L * m)
+        tmax = _d()
+        res = np.zeros_like(pos)
+        self._check(self.lib.im_run_multilevel(
+            self.h, _dp(pos), _dp(tgt), n, C.byref(cfg), C.byref(nl), _szp(nc), _szp(idx),
+            _dp(alpha), _dp(ach), caph.ctypes.data_as(_pi), _dp(ltm), _dp(el), _szp(nrec),
+            _dp(rerr), C.byref(tmax), _dp(res)))
+        out = MultilevelResult(target_max=tmax.value, final_residual=res)
+        for l in range(nl.value):
+            k, r = int(nc[l]), int(nrec[l])
+            out.levels.append(LevelResult(idx[l * m:l * m + k].astype(np.int64),
+                                          alpha[l * m:l * m + k].copy(), float(ach[l]),
+                                          bool(caph[l]), float(ltm[l]), float(el[l]),
+                                          np.arange(1, r + 1), rerr[l * m:l * m + r].copy(),
+                                          None, None))
+        return out
+
+    # -- wall distance / volume ----------------------------------------------
+    def build_distance_index(self, nodes, dim, surface) -> np.ndarray:
+        nodes = xyz(nodes)
+        s = np.ascontiguousarray(np.asarray(surface, dtype=np.uint64))
+        out = np.zeros(len(nodes))
+        self._check(self.lib.im_build_distance_index(self.h, _dp(nodes), len(nodes), dim,
+                                                     _szp(s), len(s), _dp(out)))
+        return out
+
+    def update_volume(self, nodes, dist, ctrl, alpha, D, psi_kind=0, kind="c2", R=1.0,
+                      precision=FP64):
+        nodes, c, a = xyz(nodes), xyz(ctrl), xyz(alpha)
+        dist = np.ascontiguousarray(dist, dtype=np.float64)
+        if len(dist) != len(nodes):
+            raise ValueError("distance index does not match the mesh")
+        n = len(nodes)
+        idx = np.zeros(max(n, 1), np.uint64)
+        val = np.zeros((max(n, 1), 3))
+        cnt = _sz()
+        wf = WallFunctionC(1.0, D, psi_kind)
+        self._check(self.lib.im_update_volume(self.h, _dp(nodes), n, _dp(dist), _dp(c), _dp(a),
+                                              len(c), C.byref(wf), basis(kind, R), precision,
+                                              _szp(idx), _dp(val), C.byref(cnt)))
+        k = cnt.value
+        return idx[:k].astype(np.int64), val[:k].copy()
+
+    def deform(self, nodes, dim, patch, disp, pinned=(), tol=0.1, max_levels=5, cap=5000,
+               kind="c2", R=1.0, volume_k=5.0, support_distance=-1.0, psi_kind=0,
+               precision=FP64):
+        nodes, disp = xyz(nodes), xyz(disp)
+        patch = np.ascontiguousarray(patch, dtype=np.uint64)
+        pinned = np.ascontiguousarray(np.asarray(pinned, dtype=np.uint64).reshape(-1))
+        cfg = DeformConfigC(GreedyConfigC(tol, max_levels, cap, basis(kind, R)), volume_k,
+                            support_distance, psi_kind, precision)
+        rep = DeformReportC()
+        out = np.zeros_like(nodes)
+        L = max_levels
+        pts, tch = np.zeros(L, np.uint64), np.zeros(L, np.uint64)
+        ach, sup, sec = np.zeros(L), np.zeros(L), np.zeros(L)
+        caph = np.zeros(L, np.int32)
+        self._check(self.lib.im_deform(
+            self.h, _dp(nodes), len(nodes), dim, _szp(patch), len(patch), _dp(disp),
+            _szp(pinned) if len(pinned) else None, len(pinned), C.byref(cfg), _dp(out),
+            C.byref(rep), _szp(pts), _dp(ach), caph.ctypes.data_as(_pi), _dp(sup), _szp(tch),
+            _dp(sec)))
+        k = rep.n_levels
+        return dict(nodes=out, points=pts[:k].astype(np.int64), touched=tch[:k].astype(np.int64),
+                    support=sup[:k].copy(), achieved=ach[:k].copy(),
+                    cap_hit=caph[:k].astype(bool), seconds=sec[:k].copy(),
+                    target_max=rep.target_max, surface_max_error=rep.surface_max_error,
+                    surface_mean_error=rep.surface_mean_error, total_seconds=rep.total_seconds,
+                    greedy_seconds=rep.greedy_seconds, distance_seconds=rep.distance_seconds,
+                    volume_seconds=rep.volume_seconds)
+
+
+class VolumePlan:
+    """Resident volume-update plan (im_volume_plan): mesh + wall distances in
+    HBM, one call per level."""
+
+    def __init__(self, ctx: Context, nodes, dim, surface, cutoff=math.inf):
+        self.ctx = ctx
+        nodes = xyz(nodes)
+        s = np.ascontiguousarray(np.asarray(surface, dtype=np.uint64))
+        h = C.c_void_p()
+        ctx._check(ctx.lib.im_volume_plan_create(ctx.h, _dp(nodes), len(nodes), dim, _szp(s),
+                                                 len(s), cutoff, C.byref(h)))
+        self.h = h
+        self.n = len(nodes)
+
+    def set_controls(self, ctrl, alpha):
+        c, a = xyz(ctrl), xyz(alpha)
+        self.ctx._check(self.ctx.lib.im_volume_plan_set_controls(self.h, _dp(c), _dp(a), len(c)))
+
+    def run(self, D, psi_kind=0, kind="c2", R=1.0, precision=FP64):
+        wf = WallFunctionC(1.0, D, psi_kind)
+        na, ms = _sz(), _d()
+        self.ctx._check(self.ctx.lib.im_volume_plan_run(self.h, C.byref(wf), basis(kind, R),
+                                                        precision, C.byref(na), C.byref(ms)))
+        return na.value, ms.value
+
+    def reset_field(self):
+        self.ctx._check(self.ctx.lib.im_volume_plan_reset_field(self.h))
+
+    def field(self) -> np.ndarray:
+        out = np.zeros((self.n, 3))
+        self.ctx._check(self.ctx.lib.im_volume_plan_download_field(self.h, _dp(out)))
+        return out
+
+    def distances(self) -> np.ndarray:
+        out = np.zeros(self.n)
+        self.ctx._check(self.ctx.lib.im_volume_plan_distances(self.h, _dp(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.im_volume_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,453 @@
+// capi.cu — the extern "C" boundary (include/icemorph_b200.h).
+//
+// Host orchestration only: validation with the reference's messages, the
+// H2D/D2H transfers, and the kernel sequences of volume.cu, wall_distance.cu
+// and greedy.cu.  Host arithmetic that must match the reference bit for bit
+// (max_magnitude, the SolveError distances, the surface error) is compiled
+// with -ffp-contract=off and follows the cited reference lines.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/icemorph_b200.h"
+#include "greedy.hpp"
+#include "runtime.hpp"
+
+namespace imb {
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double seconds_since(Clock::time_point t) {
+  return std::chrono::duration<double>(Clock::now() - t).count();
+}
+
+// ---- host reference arithmetic --------------------------------------------
+// vec.hpp:35-36
+double hnorm(double x, double y, double z) { return std::sqrt(x * x + y * y + z * z); }
+double hdist(const double* a, const double* b) {
+  return hnorm(a[0] - b[0], a[1] - b[1], a[2] - b[2]);
+}
+// greedy.cpp:35-39
+double max_magnitude(const double* v, size_t n) {
+  double m = 0.0;
+  for (size_t i = 0; i < n; ++i) m = std::max(m, hnorm(v[3 * i], v[3 * i + 1], v[3 * i + 2]));
+  return m;
+}
+// rbf.cpp:28-50
+double h_wendland(int kind, double eta) {
+  if (eta >= 1.0) return 0.0;
+  const double u = 1.0 - eta;
+  switch (kind) {
+    case 0: return u * u;
+    case 1: {
+      const double u2 = u * u;
+      return u2 * u2 * (4.0 * eta + 1.0);
+    }
+    case 2: {
+      const double u2 = u * u;
+      const double u6 = u2 * u2 * u2;
+      return u6 * ((35.0 / 3.0) * eta * eta + 6.0 * eta + 1.0);
+    }
+    case 3: {
+      const double u2 = u * u;
+      const double u8 = u2 * u2 * u2 * u2;
+      return u8 * (32.0 * eta * eta * eta + 25.0 * eta * eta + 8.0 * eta + 1.0);
+    }
+  }
+  return 0.0;
+}
+
+void check_kind(int kind) {
+  if (kind < 0 || kind > 3)
+    throw InvalidArgument("unknown basis function (expected c0, c2, c4 or c6)");
+}
+
+// greedy.cpp:20-33
+void check_config(const im_greedy_config& c) {
+  if (!(c.tolerance > 0.0 && c.tolerance < 1.0))
+    throw InvalidArgument("greedy tolerance must lie in (0,1)");
+  if (c.max_levels < 1) throw InvalidArgument("at least one level is required");
+  if (c.max_points_per_level < 1) throw InvalidArgument("per-level point cap must be positive");
+  if (!(c.basis.support_radius > 0.0))
+    throw InvalidArgument("basis support radius must be positive");
+  check_kind(c.basis.kind);
+}
+
+std::string fmt_f(double v) { return std::to_string(v); }  // std::to_string == "%f"
+
+// greedy.cpp:41-56
+[[noreturn]] void throw_conditioning_nodes(const double* pos, const std::vector<int>& controls,
+                                           size_t failed) {
+  size_t nearest = failed;
+  double best = INFINITY;
+  for (int c : controls) {
+    const double d = hdist(pos + 3 * (size_t)c, pos + 3 * failed);
+    if (d < best) best = d, nearest = (size_t)c;
+  }
+  throw SolveFailure("ill-conditioned control set: surface nodes " + std::to_string(nearest) +
+                     " and " + std::to_string(failed) + " are too close (distance " +
+                     fmt_f(best) + ")");
+}
+
+// rbf.cpp:125-140
+[[noreturn]] void throw_conditioning_points(const double* pts, size_t failed) {
+  size_t nearest = 0;
+  double best = INFINITY;
+  for (size_t i = 0; i < failed; ++i) {
+    const double d = hdist(pts + 3 * i, pts + 3 * failed);
+    if (d < best) best = d, nearest = i;
+  }
+  throw SolveFailure("ill-conditioned control set: points " + std::to_string(nearest) + " and " +
+                     std::to_string(failed) + " are too close (distance " + fmt_f(best) + ")");
+}
+
+template <class F>
+int guarded(im_context* ctx, F&& f) {
+  if (!ctx) return IM_INVALID_ARGUMENT;
+  Context& c = ctx->c;
+  try {
+    IMB_CHECK(cudaSetDevice(c.device));
+    f(c);
+    c.status = IM_OK;
+    c.message[0] = 0;
+  } catch (const InvalidArgument& e) {
+    c.status = IM_INVALID_ARGUMENT;
+    std::snprintf(c.message, sizeof c.message, "%s", e.what());
+  } catch (const std::invalid_argument& e) {
+    c.status = IM_INVALID_ARGUMENT;
+    std::snprintf(c.message, sizeof c.message, "%s", e.what());
+  } catch (const SolveFailure& e) {
+    c.status = IM_SOLVE_ERROR;
+    std::snprintf(c.message, sizeof c.message, "%s", e.what());
+  } catch (const std::exception& e) {
+    c.status = IM_RUNTIME_ERROR;
+    std::snprintf(c.message, sizeof c.message, "%s", e.what());
+  }
+  return c.status;
+}
+
+struct EventTimer {
+  cudaEvent_t a, b;
+  cudaStream_t s;
+  explicit EventTimer(cudaStream_t st) : s(st) {
+    IMB_CHECK(cudaEventCreate(&a));
+    IMB_CHECK(cudaEventCreate(&b));
+    IMB_CHECK(cudaEventRecord(a, s));
+  }
+  double stop() {
+    IMB_CHECK(cudaEventRecord(b, s));
+    IMB_CHECK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    IMB_CHECK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+  }
+  ~EventTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+// One greedy level on an engine whose target is already set.
+struct LevelOut {
+  int nc = 0, steps = 0, status = 0;
+  double achieved = 0, target_max = 0, elapsed = 0;
+};
+
+LevelOut run_engine_level(GreedyEngine& eng, const double* host_pos, const im_greedy_config& cfg,
+                          double target_max) {
+  const auto t0 = Clock::now();
+  eng.reset(cfg.tolerance, target_max, cfg.basis.kind, cfg.basis.support_radius);
+  const GState& s = eng.run_level();
+  LevelOut o;
+  o.status = s.status;
+  o.nc = s.nc;
+  o.steps = s.steps;
+  o.achieved = s.achieved;
+  o.target_max = target_max;
+  if (s.status == kStatusSolveError) {
+    std::vector<size_t> idx(s.nc);
+    eng.download(s.nc, idx.data(), nullptr, nullptr, nullptr, nullptr, 0);
+    std::vector<int> ctl(idx.begin(), idx.end());
+    throw_conditioning_nodes(host_pos, ctl, (size_t)s.fail_node);
+  }
+  o.elapsed = seconds_since(t0);
+  return o;
+}
+
+void validate_target(const double* t, size_t n) {
+  for (size_t i = 0; i < 3 * n; ++i)
+    if (!std::isfinite(t[i])) throw InvalidArgument("target displacement is not finite");
+}
+
+}  // namespace
+}  // namespace imb
+
+using namespace imb;
+
+extern "C" {
+
+const char* im_version(void) { return "icemorph-b200 0.1 (sm_100a)"; }
+
+int im_context_create(im_context** out, int device) {
+  if (!out) return IM_INVALID_ARGUMENT;
+  *out = nullptr;
+  auto* ctx = new (std::nothrow) im_context();
+  if (!ctx) return IM_RUNTIME_ERROR;
+  ctx->c.device = device;
+  int rc = guarded(ctx, [&](Context& c) {
+    IMB_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    cudaDeviceProp prop;
+    IMB_CHECK(cudaGetDeviceProperties(&prop, device));
+    c.num_sms = prop.multiProcessorCount;
+    if (prop.major != 10)
+      throw std::runtime_error("icemorph-b200 requires an sm_100 (Blackwell B200) device");
+  });
+  *out = ctx;  // returned even on failure so im_last_error can be read
+  return rc;
+}
+
+int im_context_destroy(im_context* ctx) {
+  if (!ctx) return IM_OK;
+  if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+  delete ctx;
+  return IM_OK;
+}
+
+const char* im_last_error(const im_context* ctx) { return ctx ? ctx->c.message : "null context"; }
+double im_last_device_ms(const im_context* ctx) { return ctx ? ctx->c.last_kernel_ms : 0.0; }
+
+double im_eval_wendland(int kind, double eta) { return h_wendland(kind, eta); }
+double im_eval_basis(im_basis b, double distance) {
+  return h_wendland(b.kind, distance / b.support_radius);
+}
+
+// wall_distance.cpp:33-38
+int im_make_wall_function(double k, double level_target_max, im_wall_function* out) {
+  if (!(k > 0.0)) return IM_INVALID_ARGUMENT;
+  out->reduction_factor = k;
+  out->support_distance = k * level_target_max;
+  out->psi_kind = IM_PSI_LINEAR;
+  return IM_OK;
+}
+
+// wall_distance.cpp:40-44 (+ the Wendland-C2 taper)
+double im_eval_wall_function(const im_wall_function* wf, double d) {
+  if (wf->support_distance <= 0.0) return d == 0.0 ? 1.0 : 0.0;
+  const double xi = d / wf->support_distance;
+  if (wf->psi_kind == IM_PSI_WENDLAND_C2) return h_wendland(1, xi);
+  return xi < 1.0 ? 1.0 - xi : 0.0;
+}
+
+int im_solve_weights(im_context* ctx, const double* points, const double* disp, size_t n,
+                     im_basis basis, double* alpha_out) {
+  return guarded(ctx, [&](Context& c) {
+    check_kind(basis.kind);
+    std::fill(alpha_out, alpha_out + 3 * n, 0.0);
+    if (n == 0) return;
+    bool all_zero = true;  // rbf.cpp:156-163
+    for (size_t i = 0; i < 3 * n && all_zero; ++i) all_zero = disp[i] == 0.0;
+    if (all_zero) return;
+    GreedyEngine eng(c, (int)n, (int)n);
+    eng.set_positions(points);
+    eng.set_target(disp);
+    eng.reset(0.5, 0.0, basis.kind, basis.support_radius);
+    EventTimer tm(c.stream);
+    const GState& s = eng.factor_all_and_solve();
+    c.last_kernel_ms = tm.stop();
+    if (s.status == kStatusSolveError) throw_conditioning_points(points, (size_t)s.fail_row);
+    eng.download((int)n, nullptr, alpha_out, nullptr, nullptr, nullptr, 0);
+  });
+}
+
+int im_eval_interpolant(im_context* ctx, const double* ctrl, const double* alpha, size_t nc,
+                        im_basis basis, const double* queries, size_t nq, int precision,
+                        double* out) {
+  return guarded(ctx, [&](Context& c) {
+    check_kind(basis.kind);
+    if (nq == 0) return;
+    DPoints q;
+    upload_points(c, queries, nq, q);
+    const size_t np = ctrl_padded(nc);
+    DBuf<double> staging, tiles, dout;
+    staging.reserve(6 * std::max<size_t>(nc, 1));
+    tiles.reserve(6 * np);
+    dout.reserve(3 * nq);
+    if (nc) {
+      IMB_CHECK(cudaMemcpyAsync(staging.p, ctrl, nc * 24, cudaMemcpyHostToDevice, c.stream));
+      IMB_CHECK(cudaMemcpyAsync(staging.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice, c.stream));
+    }
+    const bool exact = precision == IM_EXACT;
+    pack_controls_aos(c, staging.p, staging.p + 3 * nc, nc,
+                      exact ? 1.0 : 1.0 / basis.support_radius, tiles.p);
+    VolumeArgs a;
+    a.x = q.x.p, a.y = q.y.p, a.z = q.z.p;
+    a.n_active = nq;
+    a.tiles = tiles.p;
+    a.n_ctrl = nc;
+    a.R = basis.support_radius;
+    a.kind = basis.kind;
+    a.dim = 3;
+    a.precision = exact ? Precision::Exact : Precision::Fast64;
+    a.out_val = dout.p;
+    EventTimer tm(c.stream);
+    launch_volume(c, a);
+    c.last_kernel_ms = tm.stop();
+    IMB_CHECK(cudaMemcpy(out, dout.p, nq * 24, cudaMemcpyDeviceToHost));
+  });
+}
+
+int im_greedy_level(im_context* ctx, const double* pos, const double* target, size_t n,
+                    const im_greedy_config* cfg, size_t level_index, size_t* control_indices,
+                    double* alpha, size_t* n_controls, double* achieved_error, int* cap_hit,
+                    double* target_max, double* elapsed_seconds, size_t* record_points,
+                    double* record_error, double* record_seconds, size_t* n_records,
+                    double* residual) {
+  (void)level_index;
+  return guarded(ctx, [&](Context& c) {
+    check_config(*cfg);
+    if (n == 0) throw InvalidArgument("surface point set is empty");
+    validate_target(target, n);
+    const double tmax = max_magnitude(target, n);
+    const int cap = (int)std::min<size_t>(cfg->max_points_per_level, n);
+    GreedyEngine eng(c, (int)n, cap);
+    eng.set_positions(pos);
+    eng.set_target(target);
+    EventTimer tm(c.stream);
+    LevelOut o = run_engine_level(eng, pos, *cfg, tmax);
+    c.last_kernel_ms = tm.stop();
+    std::vector<double> sec(o.steps);
+    eng.download(o.nc, control_indices, alpha, residual, record_error,
+                 record_seconds ? record_seconds : sec.data(), o.steps);
+    *n_controls = o.nc;
+    *achieved_error = o.achieved;
+    *cap_hit = o.status == kStatusCapHit ? 1 : 0;
+    *target_max = tmax;
+    if (elapsed_seconds) *elapsed_seconds = o.elapsed;
+    if (record_points)
+      for (int s = 0; s < o.steps; ++s) record_points[s] = (size_t)s + 1;
+    *n_records = o.steps;
+  });
+}
+
+int im_run_multilevel(im_context* ctx, const double* pos, const double* target, size_t n,
+                      const im_greedy_config* cfg, size_t* n_levels, size_t* n_controls,
+                      size_t* control_indices, double* alpha, double* achieved_error,
+                      int* cap_hit, double* level_target_max, double* elapsed_seconds,
+                      size_t* n_records, double* record_error, double* target_max,
+                      double* final_residual) {
+  return guarded(ctx, [&](Context& c) {
+    check_config(*cfg);
+    const double tmax = max_magnitude(target, n);
+    *target_max = tmax;
+    if (n == 0) throw InvalidArgument("surface point set is empty");
+    validate_target(target, n);
+    const size_t m = std::min<size_t>(cfg->max_points_per_level, n);
+    const double threshold = std::pow(cfg->tolerance, (double)cfg->max_levels) * tmax;
+    GreedyEngine eng(c, (int)n, (int)m);
+    eng.set_positions(pos);
+    eng.set_target(target);
+    std::vector<double> current(target, target + 3 * n);
+    EventTimer tm(c.stream);
+    size_t nl = 0;
+    for (size_t l = 0; l < cfg->max_levels; ++l) {
+      const double cur_max = max_magnitude(current.data(), n);
+      if (l > 0 && (cur_max == 0.0 || cur_max < threshold)) break;  // greedy.cpp:187
+      if (l > 0) eng.target_from_residual();
+      LevelOut o = run_engine_level(eng, pos, *cfg, cur_max);
+      eng.download(o.nc, control_indices + l * m, alpha + 3 * l * m, current.data(),
+                   record_error ? record_error + l * m : nullptr, nullptr, o.steps);
+      n_controls[l] = o.nc;
+      achieved_error[l] = o.achieved;
+      cap_hit[l] = o.status == kStatusCapHit ? 1 : 0;
+      level_target_max[l] = cur_max;
+      if (elapsed_seconds) elapsed_seconds[l] = o.elapsed;
+      n_records[l] = o.steps;
+      ++nl;
+    }
+    c.last_kernel_ms = tm.stop();
+    *n_levels = nl;
+    if (final_residual) std::memcpy(final_residual, current.data(), 24 * n);
+  });
+}
+
+int im_build_distance_index(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
+                            const size_t* surface, size_t n_surface, double* out) {
+  return guarded(ctx, [&](Context& c) {
+    if (n_surface == 0) throw InvalidArgument("cannot build a distance index for an empty patch");
+    if (dim != 2 && dim != 3) throw InvalidArgument("kd-tree dim must be 2 or 3");
+    for (size_t i = 0; i < n_surface; ++i)
+      if (surface[i] >= n_nodes) throw InvalidArgument("surface node index out of range");
+    DPoints dn, ds;
+    upload_points(c, nodes, n_nodes, dn);
+    upload_points_indexed(c, nodes, surface, n_surface, ds);
+    DBuf<double> d;
+    d.reserve(n_nodes);
+    EventTimer tm(c.stream);
+    wall_distance(c, dn, n_nodes, ds, n_surface, dim, INFINITY, d.p);
+    c.last_kernel_ms = tm.stop();
+    IMB_CHECK(cudaMemcpy(out, d.p, n_nodes * 8, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n_surface; ++i) out[surface[i]] = 0.0;  // wall_distance.cpp:29
+  });
+}
+
+int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const double* dist,
+                     const double* ctrl, const double* alpha, size_t nc,
+                     const im_wall_function* wf, im_basis basis, int precision,
+                     size_t* entry_nodes, double* entry_values, size_t* n_entries) {
+  return guarded(ctx, [&](Context& c) {
+    check_kind(basis.kind);
+    *n_entries = 0;
+    const double D = wf->support_distance;
+    if (D <= 0.0 || n_nodes == 0) return;  // wall_distance.cpp:54
+    DPoints dn;
+    upload_points(c, nodes, n_nodes, dn);
+    DBuf<double> dd, staging, tiles, vals;
+    DBuf<uint32_t> active;
+    dd.reserve(n_nodes);
+    active.reserve(n_nodes);
+    IMB_CHECK(cudaMemcpyAsync(dd.p, dist, n_nodes * 8, cudaMemcpyHostToDevice, c.stream));
+    staging.reserve(6 * std::max<size_t>(nc, 1));
+    tiles.reserve(6 * ctrl_padded(nc));
+    if (nc) {
+      IMB_CHECK(cudaMemcpyAsync(staging.p, ctrl, nc * 24, cudaMemcpyHostToDevice, c.stream));
+      IMB_CHECK(cudaMemcpyAsync(staging.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice, c.stream));
+    }
+    const bool exact = precision == IM_EXACT;
+    EventTimer tm(c.stream);
+    pack_controls_aos(c, staging.p, staging.p + 3 * nc, nc,
+                      exact ? 1.0 : 1.0 / basis.support_radius, tiles.p);
+    const size_t na = compact_active(c, dd.p, n_nodes, D, active.p);
+    vals.reserve(3 * std::max<size_t>(na, 1));
+    VolumeArgs a;
+    a.x = dn.x.p, a.y = dn.y.p, a.z = dn.z.p;
+    a.active = active.p;
+    a.n_active = na;
+    a.dist = dd.p;
+    a.D = D;
+    a.psi_kind = wf->psi_kind;
+    a.tiles = tiles.p;
+    a.n_ctrl = nc;
+    a.R = basis.support_radius;
+    a.kind = basis.kind;
+    a.dim = 3;
+    a.precision = exact ? Precision::Exact : Precision::Fast64;
+    a.out_val = vals.p;
+    launch_volume(c, a);
+    c.last_kernel_ms = tm.stop();
+    std::vector<uint32_t> idx(na);
+    if (na) {
+      IMB_CHECK(cudaMemcpyAsync(idx.data(), active.p, na * 4, cudaMemcpyDeviceToHost, c.stream));
+      IMB_CHECK(cudaMemcpyAsync(entry_values, vals.p, na * 24, cudaMemcpyDeviceToHost, c.stream));
+      IMB_CHECK(cudaStreamSynchronize(c.stream));
+    }
+    for (size_t i = 0; i < na; ++i) entry_nodes[i] = idx[i];
+    *n_entries = na;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,554 @@
+// greedy.cu — K2..K5: multi-level greedy control-point selection with the
+// incremental Cholesky factorisation (north-star b, c).
+//
+// Reference: greedy_level (greedy.cpp:60-170), insert_control (:86-112),
+// CholeskyFactor::append / solve (rbf.cpp:71-121), run_multilevel (:172-195),
+// solve_weights (rbf.cpp:144-193).
+//
+// Every greedy step is three kernels on the context stream, with no host
+// round trip (the host only polls the device status word every kBatch steps):
+//
+//   k_insert   (1 CTA)  column phi(c_m, p_new) in control order, the new row
+//                       of L by forward substitution in the reference order
+//                       (right-looking: s_j -= L_jm r_m for m ascending, which
+//                       applies the subtractions to each s_j in exactly the
+//                       order of rbf.cpp:84), pivot + the 1e-14 SolveError
+//                       test, and the incremental forward solve y_k (the
+//                       reference recomputes y_0..y_{k-1} with identical
+//                       operations, so caching them is bit-exact).
+//   k_backward (1 warp) L^T x = y for the three axes in the reference order
+//                       (rbf.cpp:114-120): the dependent-subtraction chain of
+//                       ~k^2/2 DSUBs (8 cycles each on B200, tools/fp64_probe)
+//                       with the products formed 32-wide by the warp.
+//   k_sweep    (grid)   f_i = sum_m alpha_m phi(p_i, c_m) in control order for
+//                       every surface node, E_i = t_i - f_i, |E_i|, block then
+//                       grid argmax over unselected nodes (ties -> lowest
+//                       index, strict > of greedy.cpp:137), overall max, the
+//                       stop / cap decision of greedy.cpp:141-152.
+//
+// All arithmetic is the exact family of common.cuh, so control indices,
+// alpha, the residual and the convergence record are bit-identical to the
+// reference.  L is stored column-major packed (column i = rows i..cap-1
+// contiguous) because both the append and the backward chain walk columns.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <string>
+
+#include "common.cuh"
+#include "greedy.hpp"
+
+namespace imb {
+
+namespace {
+
+constexpr int kInsertThreads = 1024;
+constexpr int kMaxCap = 8192;  // ring[2] + rr in shared memory
+constexpr int kSweepThreads = 64;
+constexpr int kSweepTile = 128;
+
+__device__ __forceinline__ size_t colstart(size_t i, size_t cap) {
+  return i * cap - i * (i - 1) / 2;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// k_insert: greedy.cpp:86-112 / rbf.cpp:71-100
+//
+// Shared memory: rr[cap] (running s_j, then row[j]) | ring[2][cap] (columns
+// m, m+1 of L, streamed by cp.async: every thread copies exactly the rows it
+// owns, so cp.async.wait_group alone orders the copy before its own use) |
+// dg[cap] (diag + reciprocal, staged when g.ins_dg_in_smem).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kInsertThreads) k_insert(GView g) {
+  GState& st = *g.st;
+  if (st.status != 0) return;
+  extern __shared__ double sh[];
+  const size_t cap = g.cap;
+  double* rr = sh;                   // [cap]
+  double* ring = sh + cap;           // [2][cap]
+  double2* dgs = reinterpret_cast<double2*>(sh + 3 * cap);  // [cap] if staged
+  const int tid = threadIdx.x;
+  const int k = st.nc;
+  const int node = st.next;
+  if (k == 0 && tid == 0) st.t0 = globaltimer();
+
+  const double px = g.px[node], py = g.py[node], pz = g.pz[node];
+  const exact::Recip rR = exact::make_recip(g.R);
+  const double2* dg = g.diag;
+  if (g.ins_dg_in_smem) {
+    for (int j = tid; j < k; j += kInsertThreads) dgs[j] = g.diag[j];
+    dg = dgs;
+  }
+  // column (greedy.cpp:87-93 / rbf.cpp:167-170): phi(distance(c_m, p_new))
+  for (int j = tid; j < k; j += kInsertThreads) {
+    const double d = exact::dist(g.cx[j], g.cy[j], g.cz[j], px, py, pz);
+    rr[j] = exact::wendland_rt(g.kind, exact::div_rcp(d, rR));
+  }
+  // Right-looking forward substitution (rbf.cpp:80-87): once row[m] is final,
+  // every s_j (j > m) does s_j -= L_jm * row[m], so each s_j receives its
+  // subtractions in ascending m exactly as in the reference's inner loop.
+  auto issue = [&](int m) {
+    if (m < k) {
+      const double* col = g.Lt + colstart(m, cap);
+      double* dst = ring + (m & 1) * cap;
+      for (int j = m + 1 + ((tid - (m + 1)) % kInsertThreads + kInsertThreads) % kInsertThreads;
+           j < k; j += kInsertThreads)
+        cp_async8(dst + j, col + (j - m));
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  __syncthreads();
+  for (int m = 0; m < k; ++m) {
+    if ((m % kInsertThreads) == tid) {
+      const double2 dm = dg[m];
+      rr[m] = exact::div_rcp(rr[m], exact::Recip{dm.x, dm.y});  // row[j] = s / lj[j]
+    }
+    issue(m + 1);
+    cp_async_wait1();  // my copies of column m have landed
+    __syncthreads();
+    const double r = rr[m];
+    const double* lc = ring + (m & 1) * cap;
+    for (int j = m + 1 + ((tid - (m + 1)) % kInsertThreads + kInsertThreads) % kInsertThreads;
+         j < k; j += kInsertThreads)
+      rr[j] = exact::sub(rr[j], exact::mul(lc[j], r));
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  // stage y_0..y_{k-1} for the forward chain in the ring space when it fits
+  const double *yxs = g.yx, *yys = g.yy, *yzs = g.yz;
+  if (g.ins_y_in_smem) {
+    double* ys = sh + cap;
+    for (int j = tid; j < k; j += kInsertThreads)
+      ys[j] = g.yx[j], ys[cap + j] = g.yy[j], ys[2 * cap + j] = g.yz[j];
+    yxs = ys, yys = ys + cap, yzs = ys + 2 * cap;
+  }
+  __syncthreads();
+  // sq (rbf.cpp:86) and the forward solve of the new row (rbf.cpp:107-112 for
+  // i = k), both sequential chains; 4 independent chains interleaved.
+  if (tid == 0) {
+    double sq = 0.0;
+    double yx = g.tx[node], yy = g.ty[node], yz = g.tz[node];  // rhs_k = target[c_k]
+#pragma unroll 8
+    for (int j = 0; j < k; ++j) {
+      const double r = rr[j];
+      sq = exact::add(sq, exact::mul(r, r));
+      yx = exact::sub(yx, exact::mul(r, yxs[j]));
+      yy = exact::sub(yy, exact::mul(r, yys[j]));
+      yz = exact::sub(yz, exact::mul(r, yzs[j]));
+    }
+    const double diag = 1.0;  // column[k] = 1.0 (greedy.cpp:93)
+    st.max_diag = (st.max_diag < diag) ? diag : st.max_diag;
+    const double pivot_sq = exact::sub(diag, sq);
+    const double pivot = pivot_sq > 0.0 ? __dsqrt_rn(pivot_sq) : 0.0;
+    if (!(pivot > exact::mul(1e-14, st.max_diag))) {
+      st.status = kStatusSolveError;
+      st.fail_node = node;
+      st.fail_row = k;
+      st.fail_pivot = pivot;
+    } else {
+      const exact::Recip pr = exact::make_recip(pivot);
+      g.diag[k] = make_double2(pivot, pr.y);
+      g.Lt[colstart(k, cap)] = pivot;
+      g.yx[k] = exact::div_rcp(yx, pr);
+      g.yy[k] = exact::div_rcp(yy, pr);
+      g.yz[k] = exact::div_rcp(yz, pr);
+      if (k == 0 || pivot < st.smallest_pivot) st.smallest_pivot = pivot;
+      g.cidx[k] = node;
+      g.cx[k] = px, g.cy[k] = py, g.cz[k] = pz;
+      g.sel[node] = 1;
+      st.nc = k + 1;
+    }
+  }
+  __syncthreads();
+  if (st.status != 0) return;
+  // scatter the new row into the columns: L_kj at column j, offset k - j
+  for (int j = tid; j < k; j += kInsertThreads) g.Lt[colstart(j, cap) + (k - j)] = rr[j];
+}
+
+// ---------------------------------------------------------------------------
+// k_backward: rbf.cpp:114-120 for x, y, z (greedy.cpp:106-111).
+//
+// One warp walks the chunks (column i, rows j0..j0+31) of L^T in the
+// reference order.  Per chunk the 32 lanes form the products L_ji * x_j for
+// the three axes (register prefetch of L two chunks ahead), then EVERY lane
+// runs the same 32-long dependent subtraction chain from a shared-memory
+// broadcast, fully unrolled so the loads run ahead of the 8-cycle DSUBs.
+// Padding rows beyond n contribute +0.0, an exact identity for subtraction.
+// ---------------------------------------------------------------------------
+struct Chunk {
+  int i, j0;
+};
+__device__ __forceinline__ Chunk next_chunk(Chunk c, int n) {
+  if (c.j0 + 32 < n) return {c.i, c.j0 + 32};
+  return {c.i - 1, c.i};
+}
+
+__global__ void __launch_bounds__(32) k_backward(GView g) {
+  const GState& st = *g.st;
+  if (st.status != 0) return;
+  extern __shared__ double sh[];
+  const int lane = threadIdx.x;
+  const int n = st.nc;
+  const size_t cap = g.cap;
+  double4* ps = reinterpret_cast<double4*>(sh);  // [32] products
+  double4* xs = g.xs_global ? reinterpret_cast<double4*>(g.xs_global)
+                            : reinterpret_cast<double4*>(sh + 32 * 4);  // [n]
+  auto load_l = [&](Chunk c) -> double {
+    if (c.i < 0) return 0.0;
+    const int j = c.j0 + lane;
+    return j < n ? g.Lt[colstart(c.i, cap) + (j - c.i)] : 0.0;
+  };
+  if (n == 0) return;
+  // x_{n-1} = y_{n-1} / L_{n-1,n-1}
+  {
+    const double2 d = g.diag[n - 1];
+    const exact::Recip r{d.x, d.y};
+    if (lane == 0)
+      xs[n - 1] = make_double4(exact::div_rcp(g.yx[n - 1], r), exact::div_rcp(g.yy[n - 1], r),
+                               exact::div_rcp(g.yz[n - 1], r), 0.0);
+    __syncwarp();
+  }
+  Chunk c0{n - 2, n - 1};
+  Chunk c1 = next_chunk(c0, n), c2 = next_chunk(c1, n);
+  double l0 = load_l(c0), l1 = load_l(c1);
+  double sx = 0, sy = 0, sz = 0;
+  double ny0 = 0, ny1 = 0, ny2 = 0;
+  double2 nd = make_double2(1.0, 1.0);
+  if (c0.i >= 0) ny0 = g.yx[c0.i], ny1 = g.yy[c0.i], ny2 = g.yz[c0.i], nd = g.diag[c0.i];
+  while (c0.i >= 0) {
+    const double l2 = load_l(c2);
+    const int i = c0.i;
+    if (c0.j0 == i + 1) sx = ny0, sy = ny1, sz = ny2;  // s = x[i] (= y_i), rbf.cpp:115
+    const double2 di = nd;
+    const bool last = c0.j0 + 32 >= n;
+    if (last && i >= 1) ny0 = g.yx[i - 1], ny1 = g.yy[i - 1], ny2 = g.yz[i - 1], nd = g.diag[i - 1];
+    {
+      const int j = c0.j0 + lane;
+      double4 p = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (j < n) {
+        const double4 xv = xs[j];
+        p = make_double4(exact::mul(l0, xv.x), exact::mul(l0, xv.y), exact::mul(l0, xv.z), 0.0);
+      }
+      ps[lane] = p;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      const double4 p = ps[t];
+      sx = exact::sub(sx, p.x);
+      sy = exact::sub(sy, p.y);
+      sz = exact::sub(sz, p.z);
+    }
+    __syncwarp();
+    if (last) {
+      const exact::Recip r{di.x, di.y};
+      const double4 xv = make_double4(exact::div_rcp(sx, r), exact::div_rcp(sy, r),
+                                      exact::div_rcp(sz, r), 0.0);
+      if (lane == 0) xs[i] = xv;
+      __syncwarp();
+    }
+    c0 = c1, l0 = l1;
+    c1 = c2, l1 = l2;
+    c2 = next_chunk(c2, n);
+  }
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) {
+    const double4 xv = xs[i];
+    g.ax[i] = xv.x, g.ay[i] = xv.y, g.az[i] = xv.z;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_sweep: greedy.cpp:122-153
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void better(double& v, int& i, double v2, int i2) {
+  // max value, lowest index on ties (sequential strict '>' scan)
+  if (v2 > v || (v2 == v && i2 < i)) v = v2, i = i2;
+}
+
+__global__ void __launch_bounds__(kSweepThreads) k_sweep(GView g) {
+  GState& st = *g.st;
+  if (st.status != 0) return;
+  __shared__ double ct[kSweepTile][6];
+  __shared__ double wv[kSweepThreads / 32], wa[kSweepThreads / 32];
+  __shared__ int wi[kSweepThreads / 32];
+  __shared__ bool last;
+  const int n = g.n, nc = st.nc;
+  const int i = blockIdx.x * kSweepThreads + threadIdx.x;
+  const bool live = i < n;
+  const double px = live ? g.px[i] : 0.0, py = live ? g.py[i] : 0.0, pz = live ? g.pz[i] : 0.0;
+  const exact::Recip rR = exact::make_recip(g.R);
+  double fx = 0.0, fy = 0.0, fz = 0.0;
+  for (int m0 = 0; m0 < nc; m0 += kSweepTile) {
+    const int cnt = min(kSweepTile, nc - m0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += kSweepThreads) {
+      ct[t][0] = g.cx[m0 + t], ct[t][1] = g.cy[m0 + t], ct[t][2] = g.cz[m0 + t];
+      ct[t][3] = g.ax[m0 + t], ct[t][4] = g.ay[m0 + t], ct[t][5] = g.az[m0 + t];
+    }
+    __syncthreads();
+    if (live) {
+      for (int t = 0; t < cnt; ++t) {
+        // distance(surface_positions[i], surface_positions[controls[m]])
+        const double d = exact::dist(px, py, pz, ct[t][0], ct[t][1], ct[t][2]);
+        const double phi = exact::wendland_rt(g.kind, exact::div_rcp(d, rR));
+        if (phi != 0.0) {
+          fx = exact::add(fx, exact::mul(ct[t][3], phi));
+          fy = exact::add(fy, exact::mul(ct[t][4], phi));
+          fz = exact::add(fz, exact::mul(ct[t][5], phi));
+        }
+      }
+    }
+  }
+  double nv = -1.0, all = 0.0;
+  int ni = n;
+  if (live) {
+    const double ex = exact::sub(g.tx[i], fx), ey = exact::sub(g.ty[i], fy),
+                 ez = exact::sub(g.tz[i], fz);
+    g.rx[i] = ex, g.ry[i] = ey, g.rz[i] = ez;
+    const double nrm = exact::norm(ex, ey, ez);
+    if (!g.sel[i]) nv = nrm, ni = i;
+    all = nrm;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, nv, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, ni, o);
+    better(nv, ni, v2, i2);
+    const double a2 = __shfl_xor_sync(0xffffffffu, all, o);
+    all = (all < a2) ? a2 : all;
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) wv[w] = nv, wi[w] = ni, wa[w] = all;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 1; t < kSweepThreads / 32; ++t) {
+      better(nv, ni, wv[t], wi[t]);
+      all = (all < wa[t]) ? wa[t] : all;
+    }
+    g.bv[blockIdx.x] = nv, g.bi[blockIdx.x] = ni, g.ba[blockIdx.x] = all;
+    __threadfence();
+    const unsigned int ticket = atomicAdd(&st.ticket, 1u);
+    last = ticket == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  // final block: grid argmax + decision (greedy.cpp:136-152)
+  __threadfence();
+  double mv = -1.0, ov = 0.0;
+  int mi = n;
+  for (int b = 0; b < (int)gridDim.x; ++b) {
+    better(mv, mi, ((volatile double*)g.bv)[b], ((volatile int*)g.bi)[b]);
+    const double a = ((volatile double*)g.ba)[b];
+    ov = (ov < a) ? a : ov;
+  }
+  st.ticket = 0;
+  const double achieved = st.target_max > 0.0 ? exact::div(ov, st.target_max) : 0.0;
+  const int step = st.steps;
+  g.rec_err[step] = achieved;
+  g.rec_sec[step] = (double)(globaltimer() - st.t0) * 1e-9;
+  st.steps = step + 1;
+  st.achieved = achieved;
+  st.overall = ov;
+  if (achieved < st.tol) {
+    st.status = kStatusConverged;
+  } else if (nc >= g.cap || mi == n) {
+    st.status = kStatusCapHit;
+  } else {
+    st.next = mi;
+  }
+}
+
+// solve_weights driver step: insert node st.next = nc (points in order).
+__global__ void k_next_in_order(GView g, int n) {
+  GState& st = *g.st;
+  if (st.status != 0) return;
+  if (st.nc < n) st.next = st.nc;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap_(cap) {
+  if (cap > kMaxCap)
+    throw InvalidArgument("max_points_per_level above " + std::to_string(kMaxCap) +
+                          " is not supported by this build");
+  pos_.reserve(n);
+  tgt_.reserve(n);
+  res_.reserve(n);
+  sel_.reserve(n);
+  cpos_.reserve(cap);
+  cidx_.reserve(cap);
+  const size_t tri = (size_t)cap * (cap + 1) / 2;
+  lt_.reserve(tri);
+  diag_.reserve(cap);
+  y_.reserve(cap);
+  alpha_.reserve(cap);
+  nblk_ = (n + kSweepThreads - 1) / kSweepThreads;
+  bv_.reserve(nblk_);
+  ba_.reserve(nblk_);
+  bi_.reserve(nblk_);
+  rec_err_.reserve(cap + 1);
+  rec_sec_.reserve(cap + 1);
+  st_.reserve(1);
+  IMB_CHECK(cudaMallocHost(&hst_, sizeof(GState)));
+  // x workspace of the backward chain: shared memory when it fits
+  const size_t xs_bytes = (size_t)cap * 32 + 32 * 32;
+  if (xs_bytes <= 200 * 1024) {
+    bw_smem_ = xs_bytes;
+  } else {
+    xs_.reserve((size_t)cap * 4);
+    bw_smem_ = 32 * 32;
+  }
+  IMB_CHECK(cudaFuncSetAttribute(k_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(bw_smem_, 48 * 1024)));
+  // k_insert: rr + ring[2] (+ dg staging, which also makes room for y)
+  ins_smem_ = (size_t)cap * 24;
+  if ((size_t)cap * 40 <= 210 * 1024) ins_smem_ = (size_t)cap * 40, ins_dg_smem_ = 1;
+  ins_y_smem_ = ins_dg_smem_;
+  IMB_CHECK(cudaFuncSetAttribute(k_insert, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(ins_smem_, 48 * 1024)));
+}
+
+GreedyEngine::~GreedyEngine() {
+  if (hst_) cudaFreeHost(hst_);
+}
+
+GView GreedyEngine::view() {
+  GView g{};
+  g.st = st_.p;
+  g.n = n_;
+  g.cap = cap_;
+  g.kind = kind_;
+  g.R = R_;
+  g.px = pos_.x.p, g.py = pos_.y.p, g.pz = pos_.z.p;
+  g.tx = tgt_.x.p, g.ty = tgt_.y.p, g.tz = tgt_.z.p;
+  g.rx = res_.x.p, g.ry = res_.y.p, g.rz = res_.z.p;
+  g.sel = sel_.p;
+  g.cidx = cidx_.p;
+  g.cx = cpos_.x.p, g.cy = cpos_.y.p, g.cz = cpos_.z.p;
+  g.Lt = lt_.p;
+  g.diag = diag_.p;
+  g.yx = y_.x.p, g.yy = y_.y.p, g.yz = y_.z.p;
+  g.ax = alpha_.x.p, g.ay = alpha_.y.p, g.az = alpha_.z.p;
+  g.xs_global = xs_.p;
+  g.bv = bv_.p, g.ba = ba_.p, g.bi = bi_.p;
+  g.rec_err = rec_err_.p;
+  g.rec_sec = rec_sec_.p;
+  g.ins_y_in_smem = ins_y_smem_;
+  g.ins_dg_in_smem = ins_dg_smem_;
+  return g;
+}
+
+void GreedyEngine::set_positions(const double* host_xyz) { upload_points(ctx_, host_xyz, n_, pos_); }
+
+void GreedyEngine::set_target(const double* host_xyz) { upload_points(ctx_, host_xyz, n_, tgt_); }
+
+void GreedyEngine::target_from_residual() {
+  const size_t b = (size_t)n_ * 8;
+  IMB_CHECK(cudaMemcpyAsync(tgt_.x.p, res_.x.p, b, cudaMemcpyDeviceToDevice, ctx_.stream));
+  IMB_CHECK(cudaMemcpyAsync(tgt_.y.p, res_.y.p, b, cudaMemcpyDeviceToDevice, ctx_.stream));
+  IMB_CHECK(cudaMemcpyAsync(tgt_.z.p, res_.z.p, b, cudaMemcpyDeviceToDevice, ctx_.stream));
+}
+
+void GreedyEngine::reset(double tol, double target_max, int kind, double R) {
+  kind_ = kind;
+  R_ = R;
+  GState s{};
+  s.tol = tol;
+  s.target_max = target_max;
+  s.max_diag = 0.0;
+  s.next = 0;
+  *hst_ = s;
+  IMB_CHECK(cudaMemcpyAsync(st_.p, hst_, sizeof(GState), cudaMemcpyHostToDevice, ctx_.stream));
+  IMB_CHECK(cudaMemsetAsync(sel_.p, 0, n_, ctx_.stream));
+}
+
+const GState& GreedyEngine::poll() {
+  IMB_CHECK(cudaMemcpyAsync(hst_, st_.p, sizeof(GState), cudaMemcpyDeviceToHost, ctx_.stream));
+  IMB_CHECK(cudaStreamSynchronize(ctx_.stream));
+  return *hst_;
+}
+
+void GreedyEngine::enqueue_step(bool sweep) {
+  const GView g = view();
+  k_insert<<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);
+  k_backward<<<1, 32, bw_smem_, ctx_.stream>>>(g);
+  if (sweep)
+    k_sweep<<<nblk_, kSweepThreads, 0, ctx_.stream>>>(g);
+  else
+    k_next_in_order<<<1, 1, 0, ctx_.stream>>>(g, n_);
+  IMB_LAUNCH_CHECK();
+}
+
+const GState& GreedyEngine::run_level(int batch) {
+  for (;;) {
+    for (int b = 0; b < batch; ++b) enqueue_step(true);
+    const GState& s = poll();
+    if (s.status != kStatusRunning) return s;
+    batch = std::min(batch * 2, 256);
+  }
+}
+
+const GState& GreedyEngine::factor_all_and_solve() {
+  // solve_weights: append every point in order (rbf.cpp:165-178); only the
+  // last backward solve matters, but the intermediate ones are cheap next
+  // to the O(n^2) append at these sizes and keep one code path.
+  const GView g = view();
+  for (int k = 0; k < n_; ++k) {
+    k_insert<<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);
+    k_next_in_order<<<1, 1, 0, ctx_.stream>>>(g, n_);
+  }
+  k_backward<<<1, 32, bw_smem_, ctx_.stream>>>(g);
+  IMB_LAUNCH_CHECK();
+  return poll();
+}
+
+void GreedyEngine::download(int nc, size_t* idx, double* alpha_aos, double* residual_aos,
+                            double* rec_err, double* rec_sec, int steps) {
+  std::vector<int> ci(nc);
+  std::vector<double> ax(nc), ay(nc), az(nc);
+  if (nc) {
+    IMB_CHECK(cudaMemcpyAsync(ci.data(), cidx_.p, nc * 4, cudaMemcpyDeviceToHost, ctx_.stream));
+    IMB_CHECK(cudaMemcpyAsync(ax.data(), alpha_.x.p, nc * 8, cudaMemcpyDeviceToHost, ctx_.stream));
+    IMB_CHECK(cudaMemcpyAsync(ay.data(), alpha_.y.p, nc * 8, cudaMemcpyDeviceToHost, ctx_.stream));
+    IMB_CHECK(cudaMemcpyAsync(az.data(), alpha_.z.p, nc * 8, cudaMemcpyDeviceToHost, ctx_.stream));
+  }
+  std::vector<double> rx, ry, rz;
+  if (residual_aos) {
+    rx.resize(n_), ry.resize(n_), rz.resize(n_);
+    IMB_CHECK(cudaMemcpyAsync(rx.data(), res_.x.p, n_ * 8, cudaMemcpyDeviceToHost, ctx_.stream));
+    IMB_CHECK(cudaMemcpyAsync(ry.data(), res_.y.p, n_ * 8, cudaMemcpyDeviceToHost, ctx_.stream));
+    IMB_CHECK(cudaMemcpyAsync(rz.data(), res_.z.p, n_ * 8, cudaMemcpyDeviceToHost, ctx_.stream));
+  }
+  if (rec_err && steps)
+    IMB_CHECK(cudaMemcpyAsync(rec_err, rec_err_.p, steps * 8, cudaMemcpyDeviceToHost, ctx_.stream));
+  if (rec_sec && steps)
+    IMB_CHECK(cudaMemcpyAsync(rec_sec, rec_sec_.p, steps * 8, cudaMemcpyDeviceToHost, ctx_.stream));
+  IMB_CHECK(cudaStreamSynchronize(ctx_.stream));
+  for (int i = 0; i < nc; ++i) {
+    if (idx) idx[i] = (size_t)ci[i];
+    if (alpha_aos) alpha_aos[3 * i] = ax[i], alpha_aos[3 * i + 1] = ay[i], alpha_aos[3 * i + 2] = az[i];
+  }
+  if (residual_aos)
+    for (int i = 0; i < n_; ++i)
+      residual_aos[3 * i] = rx[i], residual_aos[3 * i + 1] = ry[i], residual_aos[3 * i + 2] = rz[i];
+}
+
+}  // namespace imb

@@ -1,0 +1,99 @@
+// greedy.hpp — device state and host driver of the exact greedy engine
+// (greedy.cu).  Internal to the library; the C-ABI is in capi.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "runtime.hpp"
+
+namespace imb {
+
+enum : int {
+  kStatusRunning = 0,
+  kStatusConverged = 1,  // achieved < tolerance (greedy.cpp:146)
+  kStatusCapHit = 2,     // cap reached or no candidate left (greedy.cpp:147-151)
+  kStatusSolveError = 3, // pivot <= 1e-14 * max_diag (rbf.cpp:92)
+};
+
+// Device-resident step state (one per level run).
+struct GState {
+  int status;
+  int nc;        // controls selected so far
+  int next;      // node inserted by the next k_insert
+  int steps;     // sweeps done (= convergence samples)
+  int fail_node, fail_row;
+  unsigned int ticket;
+  int pad;
+  double tol, target_max, max_diag, smallest_pivot, achieved, overall, fail_pivot;
+  unsigned long long t0;
+};
+
+struct GView {
+  GState* st;
+  int n, cap, kind;
+  double R;
+  const double *px, *py, *pz;  // surface positions
+  const double *tx, *ty, *tz;  // level target
+  double *rx, *ry, *rz;        // residual
+  unsigned char* sel;
+  int* cidx;
+  double *cx, *cy, *cz;        // control positions (insertion order)
+  double* Lt;                  // column-major packed lower factor
+  double2* diag;               // (L_kk, refined reciprocal)
+  double *yx, *yy, *yz;        // forward solutions
+  double *ax, *ay, *az;        // alpha
+  double* xs_global;           // backward-chain workspace when smem is too small
+  double *bv, *ba;
+  int* bi;
+  double *rec_err, *rec_sec;
+  int ins_y_in_smem;
+  int ins_dg_in_smem;
+};
+
+class GreedyEngine {
+ public:
+  GreedyEngine(Context& ctx, int n, int cap);
+  ~GreedyEngine();
+  GreedyEngine(const GreedyEngine&) = delete;
+  GreedyEngine& operator=(const GreedyEngine&) = delete;
+
+  void set_positions(const double* host_xyz);
+  void set_target(const double* host_xyz);
+  void target_from_residual();
+  void reset(double tol, double target_max, int kind, double R);
+  const GState& run_level(int batch = 8);
+  const GState& factor_all_and_solve();
+  const GState& poll();
+  void download(int nc, size_t* idx, double* alpha_aos, double* residual_aos, double* rec_err,
+                double* rec_sec, int steps);
+
+  // device views for the volume pipeline
+  const DPoints& positions() const { return pos_; }
+  const DPoints& control_positions() const { return cpos_; }
+  const DPoints& alpha() const { return alpha_; }
+  const DPoints& residual() const { return res_; }
+  int n() const { return n_; }
+  int cap() const { return cap_; }
+
+ private:
+  GView view();
+  void enqueue_step(bool sweep);
+
+  Context& ctx_;
+  int n_, cap_;
+  int kind_ = 1;
+  double R_ = 1.0;
+  int nblk_ = 1;
+  size_t bw_smem_ = 0, ins_smem_ = 0;
+  int ins_y_smem_ = 0, ins_dg_smem_ = 0;
+  DPoints pos_, tgt_, res_, cpos_, y_, alpha_;
+  DBuf<unsigned char> sel_;
+  DBuf<int> cidx_;
+  DBuf<double> lt_, xs_, bv_, ba_, rec_err_, rec_sec_;
+  DBuf<double2> diag_;
+  DBuf<int> bi_;
+  DBuf<GState> st_;
+  GState* hst_ = nullptr;
+};
+
+}  // namespace imb

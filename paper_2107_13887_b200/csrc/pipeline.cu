@@ -1,0 +1,458 @@
+// pipeline.cu — deform() orchestration on the device (pipeline.cpp:19-106)
+// and the resident volume plan used by the benchmark.
+//
+// deform: surface system = patch ++ pinned (pipeline.cpp:35-53) ->
+//         run_multilevel on the device engine (greedy.cu) ->
+//         wall distances once on the undeformed mesh, culled at the largest
+//         support distance (wall_distance.cu) ->
+//         per level: stable compaction of d < D_l, then the volume update
+//         accumulated into the resident node array in level order, pinned
+//         nodes skipped (pipeline.cpp:64-73) ->
+//         surface max/mean error (pipeline.cpp:87-99).
+// The mesh crosses PCIe once in each direction.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/icemorph_b200.h"
+#include "greedy.hpp"
+#include "runtime.hpp"
+
+namespace imb {
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t) { return std::chrono::duration<double>(Clock::now() - t).count(); }
+
+double hnorm(double x, double y, double z) { return std::sqrt(x * x + y * y + z * z); }
+double max_magnitude(const double* v, size_t n) {
+  double m = 0.0;
+  for (size_t i = 0; i < n; ++i) m = std::max(m, hnorm(v[3 * i], v[3 * i + 1], v[3 * i + 2]));
+  return m;
+}
+
+[[noreturn]] void throw_conditioning_nodes(const double* pos, const std::vector<size_t>& controls,
+                                           size_t failed) {
+  size_t nearest = failed;
+  double best = INFINITY;
+  for (size_t c : controls) {
+    const double* a = pos + 3 * c;
+    const double* b = pos + 3 * failed;
+    const double d = hnorm(a[0] - b[0], a[1] - b[1], a[2] - b[2]);
+    if (d < best) best = d, nearest = c;
+  }
+  throw SolveFailure("ill-conditioned control set: surface nodes " + std::to_string(nearest) +
+                     " and " + std::to_string(failed) + " are too close (distance " +
+                     std::to_string(best) + ")");
+}
+
+template <class F>
+int guarded(im_context* ctx, F&& f) {
+  if (!ctx) return IM_INVALID_ARGUMENT;
+  Context& c = ctx->c;
+  try {
+    IMB_CHECK(cudaSetDevice(c.device));
+    f(c);
+    c.status = IM_OK;
+    c.message[0] = 0;
+  } catch (const std::invalid_argument& e) {
+    c.status = IM_INVALID_ARGUMENT;
+    std::snprintf(c.message, sizeof c.message, "%s", e.what());
+  } catch (const SolveFailure& e) {
+    c.status = IM_SOLVE_ERROR;
+    std::snprintf(c.message, sizeof c.message, "%s", e.what());
+  } catch (const std::exception& e) {
+    c.status = IM_RUNTIME_ERROR;
+    std::snprintf(c.message, sizeof c.message, "%s", e.what());
+  }
+  return c.status;
+}
+
+bool all_z_zero(const double* xyz, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (xyz[3 * i + 2] != 0.0) return false;
+  return true;
+}
+
+struct Timer {
+  cudaEvent_t a, b;
+  cudaStream_t s;
+  explicit Timer(cudaStream_t st) : s(st) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  double ms() {
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float m = 0;
+    cudaEventElapsedTime(&m, a, b);
+    return m;
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+__global__ void k_zero_at(double* d, const unsigned long long* idx, size_t n) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[idx[i]] = 0.0;
+}
+
+__global__ void k_set_flags(unsigned char* f, const unsigned long long* idx, size_t n) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f[idx[i]] = 1;
+}
+
+__global__ void k_soa_to_aos(const double* x, const double* y, const double* z, size_t n,
+                             double* aos) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  aos[3 * i] = x[i];
+  aos[3 * i + 1] = y[i];
+  aos[3 * i + 2] = z[i];
+}
+
+}  // namespace
+}  // namespace imb
+
+using namespace imb;
+
+struct im_volume_plan {
+  im_context* ctx;
+  size_t n = 0;
+  int dim = 3;
+  DPoints nodes, field;
+  DBuf<double> dist, tiles, ctrl_stage;
+  DBuf<uint32_t> active;
+  size_t nc = 0;
+};
+
+extern "C" {
+
+int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
+              const size_t* patch, size_t n_patch, const double* disp, const size_t* pinned,
+              size_t n_pinned, const im_deform_config* cfg, double* deformed,
+              im_deform_report* rep, size_t* level_points, double* level_achieved,
+              int* level_cap_hit, double* level_support, size_t* level_touched,
+              double* level_seconds) {
+  return guarded(ctx, [&](Context& c) {
+    const auto t_start = Clock::now();
+    if (n_patch == 0) throw InvalidArgument("marker has no nodes");  // pipeline.cpp:26-28
+    const im_greedy_config& g = cfg->greedy;
+    for (size_t i = 0; i < n_patch; ++i)
+      if (patch[i] >= n_nodes) throw InvalidArgument("patch node index out of range");
+    for (size_t i = 0; i < n_pinned; ++i)
+      if (pinned[i] >= n_nodes) throw InvalidArgument("pinned node index out of range");
+    // surface system (pipeline.cpp:35-53)
+    std::vector<size_t> surf(patch, patch + n_patch);
+    std::unordered_set<size_t> used(surf.begin(), surf.end()), pin(pinned, pinned + n_pinned);
+    for (size_t i = 0; i < n_pinned; ++i)
+      if (used.insert(pinned[i]).second) surf.push_back(pinned[i]);
+    const size_t ns = surf.size();
+    std::vector<double> pos(3 * ns), tgt(3 * ns, 0.0);
+    for (size_t i = 0; i < ns; ++i) {
+      std::memcpy(&pos[3 * i], nodes + 3 * surf[i], 24);
+      if (i < n_patch && !pin.count(surf[i])) std::memcpy(&tgt[3 * i], disp + 3 * i, 24);
+    }
+    // run_multilevel (greedy.cpp:172-195) on the device engine
+    if (!(g.tolerance > 0.0 && g.tolerance < 1.0))
+      throw InvalidArgument("greedy tolerance must lie in (0,1)");
+    if (g.max_levels < 1) throw InvalidArgument("at least one level is required");
+    if (g.max_points_per_level < 1) throw InvalidArgument("per-level point cap must be positive");
+    if (!(g.basis.support_radius > 0.0)) throw InvalidArgument("basis support radius must be positive");
+    for (double v : tgt)
+      if (!std::isfinite(v)) throw InvalidArgument("target displacement is not finite");
+    const double tmax = max_magnitude(tgt.data(), ns);
+    const size_t m = std::min<size_t>(g.max_points_per_level, ns);
+    const double threshold = std::pow(g.tolerance, (double)g.max_levels) * tmax;
+    const auto t_greedy = Clock::now();
+    GreedyEngine eng(c, (int)ns, (int)m);
+    eng.set_positions(pos.data());
+    eng.set_target(tgt.data());
+    std::vector<double> current = tgt;
+    struct Lvl {
+      std::vector<size_t> idx;
+      std::vector<double> alpha;
+      double achieved, target_max, seconds;
+      bool cap_hit;
+    };
+    std::vector<Lvl> levels;
+    for (size_t l = 0; l < g.max_levels; ++l) {
+      const double cur_max = max_magnitude(current.data(), ns);
+      if (l > 0 && (cur_max == 0.0 || cur_max < threshold)) break;
+      if (l > 0) eng.target_from_residual();
+      const auto tl = Clock::now();
+      eng.reset(g.tolerance, cur_max, g.basis.kind, g.basis.support_radius);
+      const GState s = eng.run_level();
+      Lvl lv;
+      lv.idx.resize(s.nc);
+      lv.alpha.resize(3 * (size_t)s.nc);
+      if (s.status == kStatusSolveError) {
+        eng.download(s.nc, lv.idx.data(), nullptr, nullptr, nullptr, nullptr, 0);
+        throw_conditioning_nodes(pos.data(), lv.idx, (size_t)s.fail_node);
+      }
+      eng.download(s.nc, lv.idx.data(), lv.alpha.data(), current.data(), nullptr, nullptr, 0);
+      lv.achieved = s.achieved;
+      lv.cap_hit = s.status == kStatusCapHit;
+      lv.target_max = cur_max;
+      lv.seconds = since(tl);
+      levels.push_back(std::move(lv));
+    }
+    const double greedy_s = since(t_greedy);
+
+    // support distances (pipeline.cpp:66 / the absolute-D extension)
+    std::vector<double> Dl(levels.size());
+    double cutoff = 0.0;
+    for (size_t l = 0; l < levels.size(); ++l) {
+      if (cfg->support_distance >= 0.0) {
+        Dl[l] = cfg->support_distance;
+      } else {
+        if (!(cfg->volume_k > 0.0)) throw InvalidArgument("volume reduction factor must be positive");
+        Dl[l] = cfg->volume_k * levels[l].target_max;
+      }
+      cutoff = std::max(cutoff, Dl[l]);
+    }
+
+    // mesh upload and wall distances on the undeformed mesh (pipeline.cpp:61)
+    const auto t_dist = Clock::now();
+    DPoints dn, acc, ds;
+    upload_points(c, nodes, n_nodes, dn);
+    acc.reserve(n_nodes);
+    IMB_CHECK(cudaMemcpyAsync(acc.x.p, dn.x.p, n_nodes * 8, cudaMemcpyDeviceToDevice, c.stream));
+    IMB_CHECK(cudaMemcpyAsync(acc.y.p, dn.y.p, n_nodes * 8, cudaMemcpyDeviceToDevice, c.stream));
+    IMB_CHECK(cudaMemcpyAsync(acc.z.p, dn.z.p, n_nodes * 8, cudaMemcpyDeviceToDevice, c.stream));
+    upload_points_indexed(c, nodes, patch, n_patch, ds);
+    DBuf<double> dist;
+    DBuf<unsigned long long> pidx;
+    DBuf<unsigned char> pinflag;
+    dist.reserve(n_nodes);
+    pidx.reserve(std::max(n_patch, n_pinned));
+    pinflag.reserve(n_nodes);
+    const bool any_volume = cutoff > 0.0;
+    if (any_volume) {
+      if (std::isinf(cutoff)) {
+        // D = inf: every node is active and psi == 1 regardless of d
+        // (xi = d / inf = 0), so the distances are not needed.
+        IMB_CHECK(cudaMemsetAsync(dist.p, 0, n_nodes * 8, c.stream));
+      } else {
+        wall_distance(c, dn, n_nodes, ds, n_patch, dim, cutoff, dist.p);
+        std::vector<unsigned long long> pi(patch, patch + n_patch);
+        IMB_CHECK(cudaMemcpy(pidx.p, pi.data(), n_patch * 8, cudaMemcpyHostToDevice));
+        k_zero_at<<<(n_patch + 255) / 256, 256, 0, c.stream>>>(dist.p, pidx.p, n_patch);
+      }
+    }
+    IMB_CHECK(cudaMemsetAsync(pinflag.p, 0, n_nodes, c.stream));
+    if (n_pinned) {
+      std::vector<unsigned long long> pp(pinned, pinned + n_pinned);
+      IMB_CHECK(cudaMemcpy(pidx.p, pp.data(), n_pinned * 8, cudaMemcpyHostToDevice));
+      k_set_flags<<<(n_pinned + 255) / 256, 256, 0, c.stream>>>(pinflag.p, pidx.p, n_pinned);
+    }
+    IMB_CHECK(cudaStreamSynchronize(c.stream));
+    const double dist_s = since(t_dist);
+
+    // per-level volume update (pipeline.cpp:64-85)
+    const auto t_vol = Clock::now();
+    const bool planar = dim == 2 && all_z_zero(nodes, n_nodes);
+    DBuf<uint32_t> active;
+    active.reserve(n_nodes);
+    DBuf<double> stage, tiles;
+    Timer tm(c.stream);
+    for (size_t l = 0; l < levels.size(); ++l) {
+      const Lvl& lv = levels[l];
+      size_t touched = 0;
+      if (Dl[l] > 0.0) {  // wall_distance.cpp:54
+        const size_t nc = lv.idx.size();
+        std::vector<double> cp(3 * nc);
+        for (size_t i = 0; i < nc; ++i) std::memcpy(&cp[3 * i], &pos[3 * lv.idx[i]], 24);
+        stage.reserve(6 * std::max<size_t>(nc, 1));
+        tiles.reserve(6 * ctrl_padded(nc));
+        if (nc) {
+          IMB_CHECK(cudaMemcpyAsync(stage.p, cp.data(), nc * 24, cudaMemcpyHostToDevice, c.stream));
+          IMB_CHECK(cudaMemcpyAsync(stage.p + 3 * nc, lv.alpha.data(), nc * 24,
+                                    cudaMemcpyHostToDevice, c.stream));
+        }
+        const bool exact = cfg->precision == IM_EXACT;
+        pack_controls_aos(c, stage.p, stage.p + 3 * nc, nc,
+                          exact ? 1.0 : 1.0 / g.basis.support_radius, tiles.p);
+        touched = compact_active(c, dist.p, n_nodes, Dl[l], active.p);
+        VolumeArgs a;
+        a.x = dn.x.p, a.y = dn.y.p, a.z = dn.z.p;
+        a.active = active.p;
+        a.n_active = touched;
+        a.dist = dist.p;
+        a.D = Dl[l];
+        a.psi_kind = cfg->psi_kind;
+        a.tiles = tiles.p;
+        a.n_ctrl = nc;
+        a.R = g.basis.support_radius;
+        a.kind = g.basis.kind;
+        a.dim = planar ? 2 : 3;
+        a.precision = exact ? Precision::Exact : Precision::Fast64;
+        a.acc_x = acc.x.p, a.acc_y = acc.y.p, a.acc_z = acc.z.p;
+        a.pinned = n_pinned ? pinflag.p : nullptr;
+        launch_volume(c, a);
+      }
+      level_points[l] = lv.idx.size();
+      level_achieved[l] = lv.achieved;
+      level_cap_hit[l] = lv.cap_hit ? 1 : 0;
+      level_support[l] = Dl[l];
+      level_touched[l] = touched;
+      if (level_seconds) level_seconds[l] = lv.seconds;
+    }
+    c.last_kernel_ms = tm.ms();
+    DBuf<double> aos;
+    aos.reserve(3 * n_nodes);
+    k_soa_to_aos<<<(n_nodes + 255) / 256, 256, 0, c.stream>>>(acc.x.p, acc.y.p, acc.z.p, n_nodes,
+                                                               aos.p);
+    IMB_CHECK(cudaMemcpyAsync(deformed, aos.p, n_nodes * 24, cudaMemcpyDeviceToHost, c.stream));
+    IMB_CHECK(cudaStreamSynchronize(c.stream));
+    const double vol_s = since(t_vol);
+
+    // surface accuracy (pipeline.cpp:87-99)
+    double max_err = 0.0, sum_err = 0.0;
+    for (size_t i = 0; i < n_patch; ++i) {
+      const size_t nd = patch[i];
+      const double mx = deformed[3 * nd] - nodes[3 * nd], my = deformed[3 * nd + 1] - nodes[3 * nd + 1],
+                   mz = deformed[3 * nd + 2] - nodes[3 * nd + 2];
+      const double err = hnorm(disp[3 * i] - mx, disp[3 * i + 1] - my, disp[3 * i + 2] - mz);
+      max_err = std::max(max_err, err);
+      sum_err += err;
+    }
+    rep->n_levels = levels.size();
+    rep->target_max = tmax;
+    rep->surface_max_error = 0.0;
+    rep->surface_mean_error = 0.0;
+    if (tmax > 0.0) {
+      rep->surface_max_error = max_err / tmax;
+      rep->surface_mean_error = sum_err / (tmax * (double)n_patch);
+    }
+    rep->greedy_seconds = greedy_s;
+    rep->distance_seconds = dist_s;
+    rep->volume_seconds = vol_s;
+    rep->total_seconds = since(t_start);
+  });
+}
+
+int im_volume_plan_create(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
+                          const size_t* surface, size_t n_surface, double cutoff,
+                          im_volume_plan** out) {
+  *out = nullptr;
+  auto* p = new im_volume_plan();
+  p->ctx = ctx;
+  const int rc = guarded(ctx, [&](Context& c) {
+    p->n = n_nodes;
+    p->dim = dim == 2 && all_z_zero(nodes, n_nodes) ? 2 : 3;
+    upload_points(c, nodes, n_nodes, p->nodes);
+    p->field.reserve(n_nodes);
+    p->dist.reserve(n_nodes);
+    p->active.reserve(n_nodes);
+    DPoints ds;
+    upload_points_indexed(c, nodes, surface, n_surface, ds);
+    Timer tm(c.stream);
+    if (cutoff < 0.0) {  // D = inf workloads: distances unused (psi == 1)
+      IMB_CHECK(cudaMemsetAsync(p->dist.p, 0, n_nodes * 8, c.stream));
+    } else {
+      wall_distance(c, p->nodes, n_nodes, ds, n_surface, dim, cutoff, p->dist.p);
+      DBuf<unsigned long long> pidx;
+      pidx.reserve(n_surface);
+      std::vector<unsigned long long> pi(surface, surface + n_surface);
+      IMB_CHECK(cudaMemcpy(pidx.p, pi.data(), n_surface * 8, cudaMemcpyHostToDevice));
+      k_zero_at<<<(n_surface + 255) / 256, 256, 0, c.stream>>>(p->dist.p, pidx.p, n_surface);
+    }
+    c.last_kernel_ms = tm.ms();
+    for (double* f : {p->field.x.p, p->field.y.p, p->field.z.p})
+      IMB_CHECK(cudaMemsetAsync(f, 0, n_nodes * 8, c.stream));
+    IMB_CHECK(cudaStreamSynchronize(c.stream));
+  });
+  if (rc != IM_OK) {
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return IM_OK;
+}
+
+int im_volume_plan_destroy(im_volume_plan* p) {
+  delete p;
+  return IM_OK;
+}
+
+int im_volume_plan_set_controls(im_volume_plan* p, const double* ctrl, const double* alpha,
+                                size_t nc) {
+  return guarded(p->ctx, [&](Context& c) {
+    p->nc = nc;
+    p->ctrl_stage.reserve(6 * std::max<size_t>(nc, 1));
+    p->tiles.reserve(6 * ctrl_padded(nc));
+    if (nc) {
+      IMB_CHECK(cudaMemcpy(p->ctrl_stage.p, ctrl, nc * 24, cudaMemcpyHostToDevice));
+      IMB_CHECK(cudaMemcpy(p->ctrl_stage.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice));
+    }
+    (void)c;
+  });
+}
+
+int im_volume_plan_run(im_volume_plan* p, const im_wall_function* wf, im_basis basis,
+                       int precision, size_t* n_active, double* device_ms) {
+  return guarded(p->ctx, [&](Context& c) {
+    const double D = wf->support_distance;
+    *n_active = 0;
+    if (D <= 0.0) return;
+    const bool exact = precision == IM_EXACT;
+    Timer tm(c.stream);
+    pack_controls_aos(c, p->ctrl_stage.p, p->ctrl_stage.p + 3 * p->nc, p->nc,
+                      exact ? 1.0 : 1.0 / basis.support_radius, p->tiles.p);
+    const size_t na = compact_active(c, p->dist.p, p->n, D, p->active.p);
+    VolumeArgs a;
+    a.x = p->nodes.x.p, a.y = p->nodes.y.p, a.z = p->nodes.z.p;
+    a.active = p->active.p;
+    a.n_active = na;
+    a.dist = p->dist.p;
+    a.D = D;
+    a.psi_kind = wf->psi_kind;
+    a.tiles = p->tiles.p;
+    a.n_ctrl = p->nc;
+    a.R = basis.support_radius;
+    a.kind = basis.kind;
+    a.dim = p->dim;
+    a.precision = exact ? Precision::Exact : Precision::Fast64;
+    a.acc_x = p->field.x.p, a.acc_y = p->field.y.p, a.acc_z = p->field.z.p;
+    launch_volume(c, a);
+    const double ms = tm.ms();
+    c.last_kernel_ms = ms;
+    if (device_ms) *device_ms = ms;
+    *n_active = na;
+  });
+}
+
+int im_volume_plan_reset_field(im_volume_plan* p) {
+  return guarded(p->ctx, [&](Context& c) {
+    for (double* f : {p->field.x.p, p->field.y.p, p->field.z.p})
+      IMB_CHECK(cudaMemsetAsync(f, 0, p->n * 8, c.stream));
+    IMB_CHECK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int im_volume_plan_download_field(im_volume_plan* p, double* out) {
+  return guarded(p->ctx, [&](Context& c) {
+    DBuf<double> aos;
+    aos.reserve(3 * p->n);
+    k_soa_to_aos<<<(p->n + 255) / 256, 256, 0, c.stream>>>(p->field.x.p, p->field.y.p,
+                                                            p->field.z.p, p->n, aos.p);
+    IMB_CHECK(cudaMemcpyAsync(out, aos.p, p->n * 24, cudaMemcpyDeviceToHost, c.stream));
+    IMB_CHECK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int im_volume_plan_distances(im_volume_plan* p, double* out) {
+  return guarded(p->ctx, [&](Context& c) {
+    IMB_CHECK(cudaMemcpyAsync(out, p->dist.p, p->n * 8, cudaMemcpyDeviceToHost, c.stream));
+    IMB_CHECK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,185 @@
+// runtime.hpp — host-side runtime of icemorph-b200: error types, per-call
+// context (stream + device arena), device buffers and the kernel launchers
+// each .cu file exports to the C-ABI layer (capi.cu).
+//
+// No global mutable state: every call works on an explicit Context, so two
+// contexts (e.g. two host threads) never share streams or scratch — the
+// reference's "deform is reentrant" guarantee carries over.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace imb {
+
+// Error taxonomy mirrors the reference's exceptions:
+//   std::invalid_argument -> InvalidArgument (status 1)
+//   icemorph::SolveError  -> SolveFailure    (status 2)
+//   CUDA / runtime        -> CudaError / std::runtime_error (status 3)
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct SolveFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  CudaError(cudaError_t e, const char* call, const char* file, int line)
+      : std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " in " + call +
+                           " (" + file + ":" + std::to_string(line) + ")") {}
+};
+
+#define IMB_CHECK(call)                                                          \
+  do {                                                                           \
+    cudaError_t e_ = (call);                                                     \
+    if (e_ != cudaSuccess) throw ::imb::CudaError(e_, #call, __FILE__, __LINE__); \
+  } while (0)
+
+#define IMB_LAUNCH_CHECK() IMB_CHECK(cudaGetLastError())
+
+// Owning device buffer (grow-only).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    release();
+    p = o.p, n = o.n;
+    o.p = nullptr, o.n = 0;
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  T* reserve(size_t count) {
+    if (count > n) {
+      release();
+      size_t bytes = (count ? count : 1) * sizeof(T);
+      IMB_CHECK(cudaMalloc(&p, bytes));
+      n = count;
+    }
+    return p;
+  }
+};
+
+// Pinned host staging buffer (grow-only).
+template <class T>
+struct HBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~HBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  T* reserve(size_t count) {
+    if (count > n) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      IMB_CHECK(cudaMallocHost(&p, (count ? count : 1) * sizeof(T)));
+      n = count;
+    }
+    return p;
+  }
+};
+
+// SoA coordinates on the device.
+struct DPoints {
+  DBuf<double> x, y, z;
+  size_t n = 0;
+  void reserve(size_t count) {
+    x.reserve(count), y.reserve(count), z.reserve(count);
+    n = count;
+  }
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int status = 0;
+  char message[2048] = {0};
+  // scratch
+  DBuf<unsigned char> scratch;
+  HBuf<unsigned char> pinned;
+  double last_kernel_ms = 0.0;
+};
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (definitions in the .cu files)
+// ---------------------------------------------------------------------------
+
+// AoS (3 doubles per point) host array -> device SoA.
+void upload_points(Context& ctx, const double* host_xyz, size_t n, DPoints& out);
+// Gather AoS host points by index list into device SoA.
+void upload_points_indexed(Context& ctx, const double* host_xyz, const size_t* idx, size_t n,
+                           DPoints& out);
+
+// Control tiles: (cx, cy, cz, ax, ay, az) per control, positions scaled by
+// 1/R for the fast path (scale = 1/R) or raw for the exact path (scale = 1).
+// Padded to a multiple of kCtrlTile with inert controls.
+constexpr int kCtrlTile = 256;
+size_t ctrl_padded(size_t n);
+void pack_controls(Context& ctx, const double* d_cx, const double* d_cy, const double* d_cz,
+                   const double* d_ax, const double* d_ay, const double* d_az, size_t n,
+                   double scale, double* d_tiles);
+
+void pack_controls_aos(Context& ctx, const double* d_ctrl_aos, const double* d_alpha_aos, size_t n,
+                       double scale, double* d_tiles);
+
+enum class Precision : int { Exact = 0, Fast64 = 1, Fast32 = 2 };
+
+struct VolumeArgs {
+  // points (SoA); optional gather list of active node ids (nullptr = identity)
+  const double *x = nullptr, *y = nullptr, *z = nullptr;
+  const uint32_t* active = nullptr;
+  size_t n_active = 0;
+  // wall distances per node (nullptr = psi == 1, i.e. D = inf)
+  const double* dist = nullptr;
+  double D = 0.0;
+  int psi_kind = 0;
+  // controls
+  const double* tiles = nullptr;  // packed (pack_controls)
+  size_t n_ctrl = 0;
+  double R = 1.0;
+  int kind = 1;
+  int dim = 3;
+  Precision precision = Precision::Fast64;
+  // outputs: either compacted AoS values (out_val[3k+c]) or accumulate into
+  // per-node SoA deltas (acc_x/y/z[node] += value), skipping pinned nodes.
+  double* out_val = nullptr;
+  double *acc_x = nullptr, *acc_y = nullptr, *acc_z = nullptr;
+  const unsigned char* pinned = nullptr;
+};
+
+void launch_volume(Context& ctx, const VolumeArgs& a);
+
+// Stable compaction of {i : dist[i] < D} (wall_distance.cpp:56-58).  Writes
+// ascending node ids to d_out and returns the count (synchronises).
+size_t compact_active(Context& ctx, const double* d_dist, size_t n, double D, uint32_t* d_out);
+
+// Exclusive scan of n u32 counts into n+1 u64 offsets (out[n] = total).
+void scan_u32_to_u64(Context& ctx, const unsigned int* in, size_t n, unsigned long long* out);
+
+// Exact wall distance (wall_distance.cpp:13-31).  cutoff = +inf for exact
+// distances everywhere; a finite cutoff lets the search stop once no surface
+// point can lie closer than cutoff (such nodes get +inf, i.e. inactive).
+void wall_distance(Context& ctx, const DPoints& nodes, size_t n_nodes, const DPoints& surface,
+                   size_t n_surface, int dim, double cutoff, double* d_out);
+
+}  // namespace imb
+
+// The opaque handle of the C-ABI (include/icemorph_b200.h).
+struct im_context {
+  imb::Context c;
+};

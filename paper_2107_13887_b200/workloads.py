@@ -1,0 +1,273 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations.
+
+None of the configurations is a public dataset: the reference paper's meshes
+are not available, so every input here is generated from the
+shapes, sizes and distributions BASELINE.json states.  The CPU oracle and the
+GPU path are always fed the *same arrays*, so parity does not depend on how
+these are generated.  Decisions on the config ambiguities:
+
+* B1 psi: cfg1 asks for a Wendland-C2 taper (``psi_kind = 1``); the others use
+  the reference's linear taper (``psi_kind = 0``).
+* B2 D: a fixed absolute support distance per config (``D``), inf allowed.
+* B3 eps: GreedyConfig.tolerance = 1e-3 / 1e-4 with the reference's per-level
+  normalisation (greedy.cpp:143).
+* B4 growth: first spacing and far field kept, the ratio solved.
+* B5 the surface is a separate point set appended after the volume nodes; its
+  indices form the deforming marker.
+* B6 closed-trailing-edge NACA0012 (coefficient -0.1036, generators.cpp:14-17).
+* B7 span along y.  B8 Gaussian exp(-s^2 / 2 sigma^2), s = arc length from the
+  leading edge (min-x node).  B9 cap 5000 (greedy.hpp:15).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass
+class Workload:
+    name: str
+    dim: int
+    nodes: np.ndarray  # (N, 3) float64, all mesh nodes (volume + surface)
+    surface: np.ndarray  # (N_s,) int64 marker node indices (greedy seed = first)
+    displacement: np.ndarray  # (N_s, 3) prescribed surface displacement
+    R: float
+    tol: float
+    levels: int
+    D: float  # absolute support distance (inf = no culling)
+    psi_kind: int = 0
+    kind: str = "c2"
+    cap: int = 5000
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n_nodes(self) -> int:
+        return len(self.nodes)
+
+
+def naca0012_half_thickness(x: np.ndarray, chord: float = 1.0) -> np.ndarray:
+    """generators.cpp:12-18 (closed trailing edge)."""
+    x = np.clip(x, 0.0, 1.0)
+    y = 0.2969 * np.sqrt(x) - 0.1260 * x - 0.3516 * x**2 + 0.2843 * x**3 - 0.1036 * x**4
+    return 5.0 * 0.12 * chord * y
+
+
+def airfoil_profile(n: int) -> np.ndarray:
+    """Cosine-spaced NACA0012 ring, trailing edge first, upper surface first
+    (generators.cpp:58-70)."""
+    j = np.arange(n)
+    theta = 2.0 * np.pi * j / n
+    x = 0.5 * (1.0 + np.cos(theta))
+    y = naca0012_half_thickness(x)
+    y = np.where(2 * j > n, -y, y)
+    y[0] = 0.0
+    if n % 2 == 0:
+        y[n // 2] = 0.0
+    return np.stack([x, y, np.zeros(n)], axis=1)
+
+
+def solve_growth(layers: int, first_fraction: float) -> float:
+    """Ratio g with (g-1)/(g^M-1) = first_fraction (generators.cpp:26-41)."""
+    lo, hi = 1.0 + 1e-12, 2.0
+    f = lambda g: (g - 1.0) / math.expm1(layers * math.log(g))
+    if f(lo) <= first_fraction:
+        return lo
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if f(mid) > first_fraction:
+            lo = mid
+        else:
+            hi = mid
+    return 0.5 * (lo + hi)
+
+
+def layer_fractions(layers: int, first_spacing: float, far: float) -> np.ndarray:
+    g = solve_growth(layers, first_spacing / far)
+    i = np.arange(1, layers + 1, dtype=np.float64)
+    return (g**i - 1.0) / (g**layers - 1.0)
+
+
+def arc_from_le(ring: np.ndarray) -> np.ndarray:
+    """Signed arc length along the closed polyline from the min-x node
+    (generators.cpp:219-284 measures from the leading edge)."""
+    n = len(ring)
+    le = int(np.argmin(ring[:, 0]))
+    seg = np.linalg.norm(np.diff(np.vstack([ring, ring[:1]]), axis=0), axis=1)
+    cum = np.concatenate([[0.0], np.cumsum(seg)])[:n]
+    s = cum - cum[le]
+    total = cum[-1] + seg[-1]
+    s = np.where(s > total / 2, s - total, s)
+    s = np.where(s < -total / 2, s + total, s)
+    return s
+
+
+def outward_normals_2d(ring: np.ndarray) -> np.ndarray:
+    t = np.roll(ring, -1, axis=0) - np.roll(ring, 1, axis=0)
+    nrm = np.stack([t[:, 1], -t[:, 0], np.zeros(len(ring))], axis=1)
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    # ring is counterclockwise from the TE along the upper surface: (ty, -tx)
+    # points outward for a clockwise ring; flip to outward by checking y>0 at
+    # the upper mid-chord node.
+    up = len(ring) // 4
+    if nrm[up, 1] < 0:
+        nrm = -nrm
+    return nrm
+
+
+def o_mesh(ring_pts: int, layers: int, first_spacing: float, far: float) -> np.ndarray:
+    prof = airfoil_profile(ring_pts)
+    theta = 2.0 * np.pi * np.arange(ring_pts) / ring_pts
+    center = np.array([0.5, 0.0, 0.0])
+    farf = center + far * np.stack([np.cos(theta), np.sin(theta), np.zeros(ring_pts)], axis=1)
+    t = layer_fractions(layers, first_spacing, far)[:, None, None]
+    vol = prof[None] * (1.0 - t) + farf[None] * t
+    return vol.reshape(-1, 3)
+
+
+def _airfoil_case(name, n_surf, ring, layers, bump, R, tol, levels, D, psi_kind, seed):
+    vol = o_mesh(ring, layers, 1e-4, 20.0)
+    surf = airfoil_profile(n_surf)
+    nodes = np.vstack([vol, surf])
+    surface = np.arange(len(vol), len(nodes), dtype=np.int64)
+    s = arc_from_le(surf)
+    disp = bump(s)[:, None] * outward_normals_2d(surf)
+    return Workload(name, 2, np.ascontiguousarray(nodes), surface, np.ascontiguousarray(disp),
+                    R, tol, levels, D, psi_kind, meta=dict(seed=seed, ring=ring, layers=layers))
+
+
+def cfg1(scale: float = 1.0) -> Workload:
+    """2D iced airfoil: 1,000 surface points, 400 x 250 O-mesh (100k), one
+    Gaussian bump (0.02c, sigma 0.01c) at the LE, R=0.5c, eps=1e-3, 2 levels,
+    D=1c, psi = Wendland C2."""
+    bump = lambda s: 0.02 * np.exp(-(s**2) / (2 * 0.01**2))
+    return _airfoil_case("cfg1_2d_iced", int(1000 * scale), int(400 * scale), int(250 * scale),
+                         bump, 0.5, 1e-3, 2, 1.0, 1, 1)
+
+
+def cfg2(scale: float = 1.0) -> Workload:
+    """2D horn ice: 10k surface points, 2000 x 500 O-mesh (1M), two horns at
+    s=+-0.03c (0.05c, sigma 0.005c) + 0.005c glaze on |s|<0.1c, R=0.25c,
+    eps=1e-4, 3 levels, D=0.5c."""
+
+    def bump(s):
+        h = 0.05 * (np.exp(-((s - 0.03) ** 2) / (2 * 0.005**2)) +
+                    np.exp(-((s + 0.03) ** 2) / (2 * 0.005**2)))
+        return h + np.where(np.abs(s) < 0.1, 0.005, 0.0)
+
+    return _airfoil_case("cfg2_2d_horn", int(10000 * scale), int(2000 * scale),
+                         int(500 * scale), bump, 0.25, 1e-4, 3, 0.5, 0, 2)
+
+
+# ---- 3D swept wing ---------------------------------------------------------
+SWEEP = math.radians(30.0)
+SEMISPAN = 4.0
+
+
+def wing_surface(n_chord: int, n_span: int):
+    """NACA0012 sections (chord 1, span along y, 30 deg sweep), n_chord points
+    around each section (TE first, upper first), n_span stations on [0, b]."""
+    prof = airfoil_profile(n_chord)
+    y = np.linspace(0.0, SEMISPAN, n_span)
+    xle = y * math.tan(SWEEP)
+    pts = np.empty((n_span, n_chord, 3))
+    pts[:, :, 0] = xle[:, None] + prof[None, :, 0]
+    pts[:, :, 1] = y[:, None]
+    pts[:, :, 2] = prof[None, :, 1]
+    return pts, prof
+
+
+def wing_volume(n_around: int, n_span: int, layers: int, first_spacing: float, far: float):
+    prof = airfoil_profile(n_around)
+    theta = 2.0 * np.pi * np.arange(n_around) / n_around
+    y = np.linspace(0.0, 2.0 * SEMISPAN, n_span)  # wing + tip/wake extension
+    yc = np.minimum(y, SEMISPAN)
+    xle = yc * math.tan(SWEEP)
+    t = layer_fractions(layers, first_spacing, far)
+    out = np.empty((layers, n_span, n_around, 3))
+    for li, tt in enumerate(t):
+        wx = xle[:, None] + prof[None, :, 0]
+        wz = np.broadcast_to(prof[None, :, 1], wx.shape)
+        fx = (xle[:, None] + 0.5) + far * np.cos(theta)[None, :]
+        fz = far * np.broadcast_to(np.sin(theta)[None, :], wx.shape)
+        out[li, :, :, 0] = wx * (1 - tt) + fx * tt
+        out[li, :, :, 1] = y[:, None]
+        out[li, :, :, 2] = wz * (1 - tt) + fz * tt
+    return out.reshape(-1, 3)
+
+
+def _wing_case(name, n_chord, n_span, vol_around, vol_span, layers, first, disp_fn, R, tol,
+               levels, D, seed):
+    spts, prof = wing_surface(n_chord, n_span)
+    vol = wing_volume(vol_around, vol_span, layers, first, 20.0)
+    surf = spts.reshape(-1, 3)
+    nodes = np.vstack([vol, surf])
+    surface = np.arange(len(vol), len(nodes), dtype=np.int64)
+    disp = disp_fn(spts, prof, np.random.default_rng(seed)).reshape(-1, 3)
+    return Workload(name, 3, np.ascontiguousarray(nodes), surface, np.ascontiguousarray(disp),
+                    R, tol, levels, D, 0, meta=dict(seed=seed))
+
+
+def _ridge(spts, prof, rng):
+    n_span, n_chord, _ = spts.shape
+    y = spts[:, 0, 1]
+    s = arc_from_le(prof)  # chordwise arc from the LE, same for every section
+    nrm2 = outward_normals_2d(prof)  # (x, z) normal of the section
+    mod = rng.uniform(0.8, 1.2, n_span)
+    w = max(1, int(round(0.1 * SEMISPAN / (SEMISPAN / max(n_span - 1, 1)))))
+    mod = np.convolve(np.pad(mod, w, mode="edge"), np.ones(2 * w + 1) / (2 * w + 1), "valid")
+    amp = 0.03 * (1.0 - 0.5 * y / SEMISPAN) * mod
+    h = amp[:, None] * np.exp(-(s[None, :] ** 2) / (2 * 0.01**2))
+    d = np.zeros_like(spts)
+    d[:, :, 0] = h * nrm2[None, :, 0]
+    d[:, :, 2] = h * nrm2[None, :, 1]
+    return d
+
+
+def _bend_twist(spts, prof, rng):
+    y = spts[:, :, 1]
+    b = SEMISPAN
+    dz = 0.1 * b * (y / b) ** 2
+    ang = np.radians(5.0) * (y / b)
+    xq = y * math.tan(SWEEP) + 0.25
+    rx, rz = spts[:, :, 0] - xq, spts[:, :, 2]
+    d = np.zeros_like(spts)
+    d[:, :, 0] = rx * np.cos(ang) + rz * np.sin(ang) - rx
+    d[:, :, 2] = -rx * np.sin(ang) + rz * np.cos(ang) - rz + dz
+    return d
+
+
+def cfg3(scale: float = 1.0) -> Workload:
+    """3D iced swept wing: 400 x 100 surface (40k), 20M volume points in 50
+    layers (ratio 1.08 -> first spacing 0.0349c), LE ridge, R=0.5c, eps=1e-3,
+    3 levels, D=1c."""
+    s = scale
+    return _wing_case("cfg3_3d_iced_wing", int(400 * s), int(100 * s), int(400 * s),
+                      int(1000 * s), 50, 0.0349, _ridge, 0.5, 1e-3, 3, 1.0, 3)
+
+
+def cfg4(scale: float = 1.0) -> Workload:
+    """3D global wing deformation: 100k surface points (500 x 200), 40M volume
+    points, bending 0.1b (y/b)^2 + twist 0..5 deg about c/4, R=10b=40,
+    eps=1e-4, 4 levels, D=inf (no culling)."""
+    s = scale
+    return _wing_case("cfg4_3d_global_wing", int(500 * s), int(200 * s), int(400 * s),
+                      int(2000 * s), 50, 0.0349, _bend_twist, 40.0, 1e-4, 4, math.inf, 4)
+
+
+def raw(n_ctrl: int, n_vol: int, R: float, D: float = math.inf, seed: int = 5,
+        n_wall: int = 10000):
+    """Raw kernel sweep inputs: controls U[0,1]^3 with alpha ~ N(0,1)^3,
+    volume points U[-0.5,1.5]^3, a 10k-point wall on the sphere r=0.5 about
+    (0.5,0.5,0.5)."""
+    rng = np.random.default_rng(seed)
+    ctrl = rng.random((n_ctrl, 3))
+    alpha = rng.standard_normal((n_ctrl, 3))
+    vol = rng.random((n_vol, 3)) * 2.0 - 0.5
+    w = rng.standard_normal((n_wall, 3))
+    wall = 0.5 + 0.5 * w / np.linalg.norm(w, axis=1, keepdims=True)
+    return dict(ctrl=ctrl, alpha=alpha, vol=vol, wall=wall, R=R, D=D)
+
+
+CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4}
