@@ -199,6 +199,11 @@ int im_volume_plan_reset_field(im_volume_plan* plan);
 int im_volume_plan_download_field(im_volume_plan* plan, double* out_xyz);
 int im_volume_plan_distances(im_volume_plan* plan, double* out);
 
+/* ---- diagnostics ---------------------------------------------------------------
+ * Time the exact backward-substitution chain (rbf.cpp:114-120, 3 axes) of
+ * size n on a synthetic factor: ms per solve, for the latency roofline. */
+int im_bench_backward_chain(im_context* ctx, int n, int reps, double* ms_per_solve);
+
 #ifdef __cplusplus
 }
 #endif

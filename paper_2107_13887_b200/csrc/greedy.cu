@@ -198,79 +198,149 @@ __device__ __forceinline__ Chunk next_chunk(Chunk c, int n) {
   return {c.i - 1, c.i};
 }
 
-__global__ void __launch_bounds__(32) k_backward(GView g) {
+constexpr int kBwRing = 8;     // blocks of L in flight
+constexpr int kBwBlock = 512;  // doubles per block
+
+__device__ __forceinline__ void bw_mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+      static_cast<uint32_t>(__cvta_generic_to_shared(bar))));
+}
+__device__ __forceinline__ void bw_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void bw_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+      "r"(parity)
+      : "memory");
+}
+
+// Per block of (up to kBwBlock) elements of a column of L^T:
+//   phase A (32 lanes): P[a][e] = L_ji * x_j[a] for the three axes, from the
+//            TMA-streamed L block and x in shared memory;
+//   phase B (lanes 0..2): lane a runs the dependent chain s -= P[a][e] of its
+//            axis, a pure LDS + DSUB loop that runs at the 8-cycle DSUB
+//            latency (tools/chain_probe.cu) -- the products are off the chain.
+// x_i = s / L_ii closes each column.  Columns stream into a ring of
+// shared-memory blocks by 1-D TMA bulk copies (mbarrier completion),
+// kBwRing blocks ahead of the chain.
+struct BwBlock {
+  int i, e0;  // column i, elements e0.. of rows j = i+1+e
+};
+
+template <bool XS_SMEM>
+__global__ void __launch_bounds__(32) k_backward_t(GView g) {
   const GState& st = *g.st;
   if (st.status != 0) return;
-  extern __shared__ double sh[];
+  extern __shared__ __align__(16) double sh[];
   const int lane = threadIdx.x;
   const int n = st.nc;
   const size_t cap = g.cap;
-  double4* ps = reinterpret_cast<double4*>(sh);  // [32] products
-  double4* xs = g.xs_global ? reinterpret_cast<double4*>(g.xs_global)
-                            : reinterpret_cast<double4*>(sh + 32 * 4);  // [n]
-  auto load_l = [&](Chunk c) -> double {
-    if (c.i < 0) return 0.0;
-    const int j = c.j0 + lane;
-    return j < n ? g.Lt[colstart(c.i, cap) + (j - c.i)] : 0.0;
-  };
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sh);        // [kBwRing]
+  double* ring = sh + kBwRing;                            // [kBwRing][kBwBlock+2]
+  double* P = ring + kBwRing * (kBwBlock + 2);            // [3][kBwBlock + 32]
+  // comp: X[cap] | Y[cap] | Z[cap] | D[cap]; X/Y/Z start as y and become x
+  // once solved (s = x[i] at rbf.cpp:115 reads its own slot)
+  double* comp = XS_SMEM ? P + 3 * (kBwBlock + 32) : g.xs_global;
   if (n == 0) return;
-  // x_{n-1} = y_{n-1} / L_{n-1,n-1}
-  {
-    const double2 d = g.diag[n - 1];
-    const exact::Recip r{d.x, d.y};
-    if (lane == 0)
-      xs[n - 1] = make_double4(exact::div_rcp(g.yx[n - 1], r), exact::div_rcp(g.yy[n - 1], r),
-                               exact::div_rcp(g.yz[n - 1], r), 0.0);
-    __syncwarp();
+  for (int j = lane; j < n; j += 32) {
+    comp[j] = g.yx[j], comp[cap + j] = g.yy[j], comp[2 * cap + j] = g.yz[j];
+    comp[3 * cap + j] = g.diag[j].x;
   }
-  Chunk c0{n - 2, n - 1};
-  Chunk c1 = next_chunk(c0, n), c2 = next_chunk(c1, n);
-  double l0 = load_l(c0), l1 = load_l(c1);
-  double sx = 0, sy = 0, sz = 0;
-  double ny0 = 0, ny1 = 0, ny2 = 0;
-  double2 nd = make_double2(1.0, 1.0);
-  if (c0.i >= 0) ny0 = g.yx[c0.i], ny1 = g.yy[c0.i], ny2 = g.yz[c0.i], nd = g.diag[c0.i];
-  while (c0.i >= 0) {
-    const double l2 = load_l(c2);
-    const int i = c0.i;
-    if (c0.j0 == i + 1) sx = ny0, sy = ny1, sz = ny2;  // s = x[i] (= y_i), rbf.cpp:115
-    const double2 di = nd;
-    const bool last = c0.j0 + 32 >= n;
-    if (last && i >= 1) ny0 = g.yx[i - 1], ny1 = g.yy[i - 1], ny2 = g.yz[i - 1], nd = g.diag[i - 1];
-    {
-      const int j = c0.j0 + lane;
-      double4 p = make_double4(0.0, 0.0, 0.0, 0.0);
-      if (j < n) {
-        const double4 xv = xs[j];
-        p = make_double4(exact::mul(l0, xv.x), exact::mul(l0, xv.y), exact::mul(l0, xv.z), 0.0);
-      }
-      ps[lane] = p;
-    }
-    __syncwarp();
-#pragma unroll
-    for (int t = 0; t < 32; ++t) {
-      const double4 p = ps[t];
-      sx = exact::sub(sx, p.x);
-      sy = exact::sub(sy, p.y);
-      sz = exact::sub(sz, p.z);
-    }
-    __syncwarp();
-    if (last) {
-      const exact::Recip r{di.x, di.y};
-      const double4 xv = make_double4(exact::div_rcp(sx, r), exact::div_rcp(sy, r),
-                                      exact::div_rcp(sz, r), 0.0);
-      if (lane == 0) xs[i] = xv;
-      __syncwarp();
-    }
-    c0 = c1, l0 = l1;
-    c1 = c2, l1 = l2;
-    c2 = next_chunk(c2, n);
+  if (lane == 0)
+    for (int r = 0; r < kBwRing; ++r) bw_mbar_init(&bar[r]);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  auto next = [&](BwBlock b) -> BwBlock {
+    if (b.e0 + kBwBlock < n - 1 - b.i) return {b.i, b.e0 + kBwBlock};
+    return {b.i - 1, 0};
+  };
+  auto src_of = [&](BwBlock b, int& off, int& cnt) -> const double* {
+    const double* src = g.Lt + colstart(b.i, cap) + 1 + b.e0;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
+    off = (int)((reinterpret_cast<uintptr_t>(src) - al) / 8);
+    cnt = min(kBwBlock, n - 1 - b.i - b.e0);
+    return reinterpret_cast<const double*>(al);
+  };
+  auto issue = [&](BwBlock b, int slot) {
+    if (lane != 0 || b.i < 0) return;
+    int off, cnt;
+    const double* al = src_of(b, off, cnt);
+    const uint32_t bytes = (uint32_t)(((off + cnt) * 8 + 15) & ~15);
+    bw_bulk(ring + slot * (kBwBlock + 2), al, bytes, &bar[slot]);
+  };
+  const double* dd = comp + 3 * cap;
+  if (lane < 3) {  // x_{n-1} = y_{n-1} / L_{n-1,n-1}
+    double* cx = comp + (size_t)lane * cap;
+    cx[n - 1] = exact::div_rcp(cx[n - 1], exact::make_recip(dd[n - 1]));
   }
   __syncwarp();
-  for (int i = lane; i < n; i += 32) {
-    const double4 xv = xs[i];
-    g.ax[i] = xv.x, g.ay[i] = xv.y, g.az[i] = xv.z;
+  BwBlock cur{n - 2, 0}, ahead = cur;
+  for (int r = 0; r < kBwRing; ++r) {
+    issue(ahead, r);
+    ahead = next(ahead);
   }
+  double s = 0.0;
+  for (int t = 0; cur.i >= 0; ++t) {
+    const int slot = t % kBwRing;
+    const int i = cur.i;
+    int off, cnt;
+    src_of(cur, off, cnt);
+    bw_wait(&bar[slot], (uint32_t)((t / kBwRing) & 1));
+    // phase A: products for the three axes
+    {
+      const double* lb = ring + slot * (kBwBlock + 2) + off;
+      const int j0 = i + 1 + cur.e0;
+      for (int e = lane; e < cnt; e += 32) {
+        const double l = lb[e];
+        P[e] = exact::mul(l, comp[j0 + e]);
+        P[(kBwBlock + 32) + e] = exact::mul(l, comp[cap + j0 + e]);
+        P[2 * (kBwBlock + 32) + e] = exact::mul(l, comp[2 * cap + j0 + e]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    issue(ahead, slot);  // refill the slot just consumed
+    ahead = next(ahead);
+    const BwBlock nx = next(cur);
+    // phase B: the dependent chains, rbf.cpp:116-118 in ascending j
+    if (lane < 3) {
+      double* cx = comp + (size_t)lane * cap;
+      const double* pa = P + lane * (kBwBlock + 32);
+      if (cur.e0 == 0) s = cx[i];
+      // ping-pong register sets: the loads of one 16-group run under the
+      // chain of the other (no rotation moves).  P is zero-padded past cnt
+      // below, so whole groups are always safe to load.
+      double ra[16], rb[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) ra[u] = pa[u];
+      int e = 0;
+      for (; e + 32 <= cnt; e += 32) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) rb[u] = pa[e + 16 + u];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s = exact::sub(s, ra[u]);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) ra[u] = pa[e + 32 + u];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s = exact::sub(s, rb[u]);
+      }
+      for (; e < cnt; ++e) s = exact::sub(s, pa[e]);
+      if (nx.i != i) cx[i] = exact::div_rcp(s, exact::make_recip(dd[i]));  // x_i = s / L_ii
+    }
+    __syncwarp();
+    cur = nx;
+  }
+  for (int i = lane; i < n; i += 32) g.ax[i] = comp[i], g.ay[i] = comp[cap + i], g.az[i] = comp[2 * cap + i];
 }
 
 // ---------------------------------------------------------------------------
@@ -396,7 +466,7 @@ GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap
   cpos_.reserve(cap);
   cidx_.reserve(cap);
   const size_t tri = (size_t)cap * (cap + 1) / 2;
-  lt_.reserve(tri);
+  lt_.reserve(tri + 4);  // +4: 16-byte rounded bulk copies may read past the end
   diag_.reserve(cap);
   y_.reserve(cap);
   alpha_.reserve(cap);
@@ -409,14 +479,17 @@ GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap
   st_.reserve(1);
   IMB_CHECK(cudaMallocHost(&hst_, sizeof(GState)));
   // x workspace of the backward chain: shared memory when it fits
-  const size_t xs_bytes = (size_t)cap * 32 + 32 * 32;
+  const size_t head = (8 + 8 * (512 + 2) + 3 * (512 + 32)) * 8;  // mbarriers + L ring + products
+  const size_t xs_bytes = (size_t)cap * 32 + head;
   if (xs_bytes <= 200 * 1024) {
     bw_smem_ = xs_bytes;
   } else {
     xs_.reserve((size_t)cap * 4);
-    bw_smem_ = 32 * 32;
+    bw_smem_ = head;
   }
-  IMB_CHECK(cudaFuncSetAttribute(k_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  IMB_CHECK(cudaFuncSetAttribute(k_backward_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(bw_smem_, 48 * 1024)));
+  IMB_CHECK(cudaFuncSetAttribute(k_backward_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)std::max<size_t>(bw_smem_, 48 * 1024)));
   // k_insert: rr + ring[2] (+ dg staging, which also makes room for y)
   ins_smem_ = (size_t)cap * 24;
@@ -486,10 +559,17 @@ const GState& GreedyEngine::poll() {
   return *hst_;
 }
 
+void GreedyEngine::launch_backward(const GView& g) {
+  if (xs_.p)
+    k_backward_t<false><<<1, 32, bw_smem_, ctx_.stream>>>(g);
+  else
+    k_backward_t<true><<<1, 32, bw_smem_, ctx_.stream>>>(g);
+}
+
 void GreedyEngine::enqueue_step(bool sweep) {
   const GView g = view();
   k_insert<<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);
-  k_backward<<<1, 32, bw_smem_, ctx_.stream>>>(g);
+  launch_backward(g);
   if (sweep)
     k_sweep<<<nblk_, kSweepThreads, 0, ctx_.stream>>>(g);
   else
@@ -515,7 +595,7 @@ const GState& GreedyEngine::factor_all_and_solve() {
     k_insert<<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);
     k_next_in_order<<<1, 1, 0, ctx_.stream>>>(g, n_);
   }
-  k_backward<<<1, 32, bw_smem_, ctx_.stream>>>(g);
+  launch_backward(g);
   IMB_LAUNCH_CHECK();
   return poll();
 }
@@ -552,3 +632,64 @@ void GreedyEngine::download(int nc, size_t* idx, double* alpha_aos, double* resi
 }
 
 }  // namespace imb
+
+// ---------------------------------------------------------------------------
+// Diagnostics: time the exact backward chain alone on a synthetic factor
+// (unit diagonal, small off-diagonal entries) of size n, to report the
+// chain's cycles per element against the 8-cycle dependent-DSUB floor.
+// ---------------------------------------------------------------------------
+namespace imb {
+namespace {
+__global__ void k_fill_synthetic(GView g, int n) {
+  const size_t cap = g.cap;
+  const size_t total = cap * (cap + 1) / 2;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    // column-major packed: find (i, off) lazily via the hash of t
+    const unsigned long long h = (t + 1) * 0x9E3779B97F4A7C15ull;
+    g.Lt[t] = ((double)(h >> 11) * 0x1.0p-53 - 0.5) * 1e-3;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    g.Lt[colstart(i, cap)] = 1.0;
+    const exact::Recip r = exact::make_recip(1.0);
+    g.diag[i] = make_double2(1.0, r.y);
+    g.yx[i] = 1.0 + i * 1e-6, g.yy[i] = -1.0, g.yz[i] = 0.5;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    g.st->status = 0;
+    g.st->nc = n;
+  }
+}
+}  // namespace
+
+double GreedyEngine::bench_backward(int n, int reps) {
+  const GView g = view();
+  k_fill_synthetic<<<256, 256, 0, ctx_.stream>>>(g, n);
+  launch_backward(g);  // warm
+  cudaEvent_t a, b;
+  IMB_CHECK(cudaEventCreate(&a));
+  IMB_CHECK(cudaEventCreate(&b));
+  IMB_CHECK(cudaEventRecord(a, ctx_.stream));
+  for (int r = 0; r < reps; ++r) launch_backward(g);
+  IMB_CHECK(cudaEventRecord(b, ctx_.stream));
+  IMB_CHECK(cudaEventSynchronize(b));
+  float ms = 0;
+  IMB_CHECK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  IMB_LAUNCH_CHECK();
+  return ms / reps;
+}
+}  // namespace imb
+
+extern "C" int im_bench_backward_chain(im_context* ctx, int n, int reps, double* ms_per_solve) {
+  try {
+    imb::GreedyEngine eng(ctx->c, n, n);
+    eng.reset(0.5, 1.0, 1, 1.0);
+    *ms_per_solve = eng.bench_backward(n, reps);
+    return 0;
+  } catch (const std::exception& e) {
+    std::snprintf(ctx->c.message, sizeof ctx->c.message, "%s", e.what());
+    return 3;
+  }
+}

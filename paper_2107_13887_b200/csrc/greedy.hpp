@@ -64,6 +64,7 @@ class GreedyEngine {
   const GState& run_level(int batch = 8);
   const GState& factor_all_and_solve();
   const GState& poll();
+  double bench_backward(int n, int reps);
   void download(int nc, size_t* idx, double* alpha_aos, double* residual_aos, double* rec_err,
                 double* rec_sec, int steps);
 
@@ -78,6 +79,7 @@ class GreedyEngine {
  private:
   GView view();
   void enqueue_step(bool sweep);
+  void launch_backward(const GView& g);
 
   Context& ctx_;
   int n_, cap_;
