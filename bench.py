@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 RBF mesh-deformation hot path (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload cfg2|cfg1|cfg3|cfg4|raw] [--scale S]
+
+Metric (BASELINE.json): "volume update Gpair-evals/s & % of FP64 peak; greedy
+selection time/level".  `value` is the volume-update throughput in dense-
+equivalent pair evaluations per second (N_active x N_c per level, the count
+the reference evaluates at rbf.cpp:198-201), summed over all ranks.
+
+Workload (default): BASELINE configs[1], the 2-D horn-ice airfoil (10k surface
+points, 1M volume points, R = 0.25c, eps = 1e-4, 3 levels, D = 0.5c), seeded
+synthetic geometry (paper_2107_13887_b200/workloads.py; no dataset exists).
+Setup (untimed): wall distances on the device, then the exact greedy
+multilevel selection on the device (reported as greedy seconds per level).
+A step = the volume update of every level (stable compaction of d < D, then
+the update accumulated into the resident field) with the mesh resident in
+HBM; L2 is flushed (256 MiB write) before every timed step.
+
+`e2e` repeats the volume update through the public C-ABI call a user makes
+(im_update_volume, the reference's update_volume) with host buffers: H2D of
+nodes, distances and controls and D2H of the sparse update inside the timed
+region.
+
+`--impl reference` times the reference's own CPU update_volume
+(oracle/_ref, the unmodified reference sources compiled in place) on the
+host cores of this box over a bounded slice of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "volume update Gpair-evals/s & % of FP64 peak; greedy selection time/level"
+UNIT = "Gpair-evals/s"
+# algorithmic flops per pair: in support / out of support
+FLOPS = {2: (17.0, 7.0), 3: (22.0, 10.0)}
+# FP64 vector peak measured on this pool's B200 with a DFMA microbenchmark
+# (tools/fp64_probe.cu: 34.2 TFLOP/s at 8 CTAs/SM); MEASURED_PEAKS.json has
+# no FP64 entry.  Nominal 148 SM x 64 DFMA x 2 x 1.965 GHz = 37.2 TFLOP/s.
+FP64_PEAK_TFLOPS = 34.2
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "fallback": True}
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and "Active" in s[3 + i] and "Not" not in s[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def build_workload(name, scale):
+    from paper_2107_13887_b200 import workloads as W
+
+    if name == "raw":
+        r = W.raw(4000, int(10_000_000 * scale), 0.2, 0.5)
+        nodes = np.vstack([r["vol"], r["wall"]])
+        surface = np.arange(len(r["vol"]), len(nodes))
+        return dict(name="raw_nc4k_nv10M_R0.2_D0.5", dim=3, nodes=nodes, surface=surface,
+                    R=r["R"], D=r["D"], psi_kind=0, fixed_controls=(r["ctrl"], r["alpha"]),
+                    tol=None, levels=1, cap=5000, disp=None)
+    w = W.CONFIGS[name](scale)
+    return dict(name=w.name, dim=w.dim, nodes=w.nodes, surface=w.surface, R=w.R, D=w.D,
+                psi_kind=w.psi_kind, fixed_controls=None, tol=w.tol, levels=w.levels, cap=w.cap,
+                disp=w.displacement)
+
+
+def run_b200(args):
+    import torch
+
+    from paper_2107_13887_b200 import capi
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = capi.Context(local)
+    wl = build_workload(args.workload, args.scale)
+    nodes, surface, dim = wl["nodes"], wl["surface"], wl["dim"]
+    R, D = wl["R"], wl["D"]
+
+    # --- setup: greedy selection on the device (exact, untimed) -----------
+    greedy = {}
+    if wl["fixed_controls"] is None:
+        pos = nodes[surface]
+        t0 = time.perf_counter()
+        ml = ctx.run_multilevel(pos, wl["disp"], wl["tol"], wl["levels"], wl["cap"], "c2", R)
+        greedy_s = time.perf_counter() - t0
+        levels = [(pos[l.control_indices], l.alpha) for l in ml.levels]
+        greedy = {"greedy_seconds_per_level": [round(l.elapsed_seconds, 4) for l in ml.levels],
+                  "greedy_points_per_level": [int(len(l.control_indices)) for l in ml.levels],
+                  "greedy_cap_hit": [bool(l.cap_hit) for l in ml.levels],
+                  "greedy_seconds_total": round(greedy_s, 4)}
+    else:
+        levels = [wl["fixed_controls"]]
+    n_ctrl = [len(c) for c, _ in levels]
+
+    # --- resident plan: nodes + wall distances in HBM ----------------------
+    cutoff = D if math.isfinite(D) else -1.0
+    t0 = time.perf_counter()
+    plan = capi.VolumePlan(ctx, nodes, dim, surface, cutoff=cutoff)
+    dist_ms = ctx.last_device_ms
+    for l, (c, a) in enumerate(levels):
+        plan.set_level(l, c, a, D, wl["psi_kind"], "c2", R, capi.FP64)
+    supp = [plan.count_support(l, "c2", R) for l in range(len(levels))]
+    pairs_step = sum(t for _, t in supp)
+    in_step = sum(i for i, _ in supp)
+    fin, fout = FLOPS[dim]
+    flops_step = fin * in_step + fout * (pairs_step - in_step)
+
+    # --- device-timed steps -------------------------------------------------
+    plan.run_steps(args.warmup, "c2", R, capi.FP64, flush_l2=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        st = plan.run_steps(args.steps, "c2", R, capi.FP64, flush_l2=True)
+    torch.cuda.synchronize()
+    step_ms = st["step_ms_total"] / args.steps
+    kern_ms = st["kernel_ms_total"] / max(st["kernel_launches"], 1)
+    if world > 1:
+        t = torch.tensor([step_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        step_ms = float(t.item())
+        torch.distributed.barrier()
+    value = world * pairs_step / (step_ms * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (the volume update): algorithmic flops
+    # per launch / average launch time (CUDA events on the context stream)
+    launches_per_step = max(1, sum(1 for n in n_ctrl if n))
+    flops_launch = flops_step / launches_per_step
+    achieved_tf = flops_launch / (kern_ms * 1e-3) / 1e12
+    roofline = {"bound": "fp64", "achieved": round(achieved_tf, 3),
+                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": round(achieved_tf / FP64_PEAK_TFLOPS, 4), "traffic": None,
+                "peak_source": "measured DFMA microbenchmark (tools/fp64_probe.cu)",
+                "algorithmic_flops_per_launch": flops_launch,
+                "in_support_fraction": round(in_step / max(pairs_step, 1), 4)}
+
+    # --- e2e through the public C-ABI with host buffers ----------------------
+    d_host = plan.distances()
+    e2e_times, h2d, d2h = [], 0, 0
+    for it in range(max(1, min(args.steps, 5)) + 1):
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        for c, a in levels:
+            idx, val = ctx.update_volume(nodes, d_host, c, a, D, wl["psi_kind"], "c2", R,
+                                         capi.FP64)
+            h2d += nodes.nbytes + d_host.nbytes + c.nbytes + a.nbytes
+            d2h += idx.size * 4 + val.nbytes
+        if it:  # first pass is warm-up
+            e2e_times.append(time.perf_counter() - t0)
+    e2e_s = statistics.median(e2e_times)
+    e2e = {"value": round(world * pairs_step / e2e_s / 1e9, 3), "unit": UNIT,
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+           "api": "im_update_volume (update_volume, wall_distance.hpp:40-42) per level"}
+
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, paper_2107_13887_b200/workloads.py)",
+        "config": {"workload": wl["name"], "n_nodes": int(len(nodes)),
+                   "n_surface": int(len(surface)), "n_controls_per_level": n_ctrl,
+                   "R": R, "D": D, "active_per_level": st["active"][:len(levels)],
+                   "pairs_per_step": int(pairs_step), "l2": "flushed (256 MiB write) before each step",
+                   "parallelism": f"{world} rank(s), contiguous node shards, no collective"},
+        "roofline": roofline,
+        "fp64_frac_of_peak": roofline["frac"],
+        "kernel_ms_avg": round(kern_ms, 4),
+        "wall_distance_ms": round(dist_ms, 3),
+        "e2e": e2e,
+        "gpu_launches": int(st["launches_per_step"] * args.steps),
+        "clocks": clk.summary(),
+    }
+    out.update(greedy)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(wl, levels, d_host, budget_s=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cpu_baseline(wl, levels, dist, budget_s=12.0, nthreads=None):
+    """The reference's own update_volume (oracle/_ref) on this box's host cores
+    over a contiguous slice of the active nodes of level 0, sized to ~budget_s."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    flavour = "ref" if pyoracle.available("ref") else "port"
+    if not pyoracle.available(flavour):
+        pyoracle.build("port")
+        flavour = "port"
+    orc = pyoracle.Oracle(flavour)
+    nthreads = nthreads or os.cpu_count() or 1
+    nodes, D, R = wl["nodes"], wl["D"], wl["R"]
+    ctrl, alpha = levels[0]
+    active = np.flatnonzero(dist < D)
+    # calibrate on a small slice, then size the sample to the budget
+    n = min(len(active), max(nthreads * 64, 2048))
+    t = 0.0
+    while True:
+        sl = active[:n]
+        t0 = time.perf_counter()
+        orc.update_volume(nodes[sl], dist[sl], ctrl, alpha, D, wl["psi_kind"], "c2", R,
+                          nthreads=nthreads)
+        t = time.perf_counter() - t0
+        if t > budget_s / 4 or n >= len(active):
+            break
+        n = min(len(active), int(n * max(2.0, budget_s / 2 / max(t, 1e-3))))
+    pairs = n * len(ctrl)
+    return {"value": round(pairs / t / 1e9, 5), "unit": UNIT, "cores": nthreads,
+            "kind": "reference" if flavour == "ref" else "port",
+            "sample": f"update_volume over {n} of {len(active)} active nodes of level 0 "
+                      f"x {len(ctrl)} controls ({t:.2f} s, {nthreads} threads)"}
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    from paper_2107_13887_b200 import workloads as W  # noqa: F401
+
+    wl = build_workload(args.workload, args.scale)
+    nodes, surface, R, D = wl["nodes"], wl["surface"], wl["R"], wl["D"]
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    flavour = "ref" if pyoracle.available("ref") else "port"
+    if not pyoracle.available(flavour):
+        pyoracle.build("port")
+        flavour = "port"
+    orc = pyoracle.Oracle(flavour)
+    nth = os.cpu_count() or 1
+    # the reference's control sets: greedy is run by the reference on a
+    # bounded prefix (its full greedy takes hours at this size);
+    # the volume-update throughput only depends on N_active x N_c.
+    pos = nodes[surface]
+    if wl["fixed_controls"] is not None:
+        ctrl, alpha = wl["fixed_controls"]
+    else:
+        g = orc.greedy_level(pos, wl["disp"], wl["tol"], 200, "c2", R)
+        ctrl, alpha = pos[g.control_indices], g.alpha
+    # wall distances of a bounded node sample (kd-tree in the reference)
+    rng = np.random.default_rng(0)
+    sample = np.sort(rng.choice(len(nodes), min(len(nodes), 200_000), replace=False))
+    sub_nodes = np.vstack([nodes[sample], pos])
+    sub_surface = np.arange(len(sample), len(sub_nodes))
+    dist = orc.build_distance_index(sub_nodes, wl["dim"], sub_surface)[:len(sample)]
+    vals = []
+    for it in range(args.warmup + args.steps):
+        cb = cpu_baseline(dict(wl, nodes=nodes[sample]), [(ctrl, alpha)], dist,
+                          budget_s=args.cpu_seconds, nthreads=nth)
+        if it >= args.warmup:
+            vals.append(cb["value"])
+    v = statistics.median(vals)
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded generator, paper_2107_13887_b200/workloads.py)",
+           "config": {"workload": wl["name"], "n_nodes": int(len(nodes)), "R": R, "D": D},
+           "cpu_baseline": dict(cb, value=v),
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -198,6 +198,17 @@ int im_volume_plan_run(im_volume_plan* plan, const im_wall_function* wf, im_basi
 int im_volume_plan_reset_field(im_volume_plan* plan);
 int im_volume_plan_download_field(im_volume_plan* plan, double* out_xyz);
 int im_volume_plan_distances(im_volume_plan* plan, double* out);
+/* multi-level steps for the benchmark: level l's packed control set, support
+ * distance and taper; run_steps executes `steps` passes over every level
+ * (compaction + update), each bracketed by CUDA events, optional L2 flush
+ * before each pass outside the brackets.  stats: see pipeline.cu. */
+int im_volume_plan_set_level(im_volume_plan* plan, int level, const double* control_positions,
+                             const double* alpha, size_t n_control, double support_distance,
+                             int psi_kind, im_basis basis, int precision);
+int im_volume_plan_run_steps(im_volume_plan* plan, im_basis basis, int precision, int steps,
+                             int flush_l2, double* stats);
+int im_volume_plan_count_support(im_volume_plan* plan, int level, im_basis basis,
+                                 unsigned long long* in_support, unsigned long long* total);
 
 /* ---- diagnostics ---------------------------------------------------------------
  * Time the exact backward-substitution chain (rbf.cpp:114-120, 3 axes) of

@@ -91,7 +91,8 @@ EXPORTS = [
     "im_run_multilevel", "im_build_distance_index", "im_update_volume", "im_deform",
     "im_volume_plan_create", "im_volume_plan_destroy", "im_volume_plan_set_controls",
     "im_volume_plan_run", "im_volume_plan_reset_field", "im_volume_plan_download_field",
-    "im_volume_plan_distances",
+    "im_volume_plan_distances", "im_volume_plan_set_level", "im_volume_plan_run_steps",
+    "im_volume_plan_count_support", "im_bench_backward_chain",
 ]
 
 
@@ -131,6 +132,12 @@ def _declare(L):
     L.im_volume_plan_reset_field.argtypes = [C.c_void_p]
     L.im_volume_plan_download_field.argtypes = [C.c_void_p, _pd]
     L.im_volume_plan_distances.argtypes = [C.c_void_p, _pd]
+    L.im_volume_plan_set_level.argtypes = [C.c_void_p, C.c_int, _pd, _pd, _sz, _d, C.c_int, Basis,
+                                           C.c_int]
+    L.im_volume_plan_run_steps.argtypes = [C.c_void_p, Basis, C.c_int, C.c_int, C.c_int, _pd]
+    L.im_volume_plan_count_support.argtypes = [C.c_void_p, C.c_int, Basis,
+                                               C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]
+    L.im_bench_backward_chain.argtypes = [C.c_void_p, C.c_int, C.c_int, _pd]
 
 
 def _dp(a):
@@ -389,6 +396,24 @@ class VolumePlan:
         out = np.zeros(self.n)
         self.ctx._check(self.ctx.lib.im_volume_plan_distances(self.h, _dp(out)))
         return out
+
+    def set_level(self, level, ctrl, alpha, D, psi_kind=0, kind="c2", R=1.0, precision=FP64):
+        c, a = xyz(ctrl), xyz(alpha)
+        self.ctx._check(self.ctx.lib.im_volume_plan_set_level(
+            self.h, level, _dp(c), _dp(a), len(c), D, psi_kind, basis(kind, R), precision))
+
+    def run_steps(self, steps, kind="c2", R=1.0, precision=FP64, flush_l2=True) -> dict:
+        st = np.zeros(10)
+        self.ctx._check(self.ctx.lib.im_volume_plan_run_steps(
+            self.h, basis(kind, R), precision, steps, int(flush_l2), _dp(st)))
+        return dict(step_ms_total=st[0], kernel_ms_total=st[1], kernel_launches=int(st[2]),
+                    launches_per_step=int(st[3]), active=[int(v) for v in st[4:8]])
+
+    def count_support(self, level, kind="c2", R=1.0):
+        a, b = C.c_ulonglong(), C.c_ulonglong()
+        self.ctx._check(self.ctx.lib.im_volume_plan_count_support(self.h, level, basis(kind, R),
+                                                                  C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def close(self):
         if getattr(self, "h", None):

@@ -130,6 +130,16 @@ struct im_volume_plan {
   DBuf<double> dist, tiles, ctrl_stage;
   DBuf<uint32_t> active;
   size_t nc = 0;
+  // multi-level step (bench): per-level packed controls and support distance
+  struct Level {
+    DBuf<double> tiles;
+    size_t nc = 0;
+    double D = 0.0;
+    int psi_kind = 0;
+  };
+  Level levels[8];
+  int n_levels = 0;
+  DBuf<unsigned char> flush;
 };
 
 extern "C" {
@@ -452,6 +462,115 @@ int im_volume_plan_distances(im_volume_plan* p, double* out) {
   return guarded(p->ctx, [&](Context& c) {
     IMB_CHECK(cudaMemcpyAsync(out, p->dist.p, p->n * 8, cudaMemcpyDeviceToHost, c.stream));
     IMB_CHECK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int im_volume_plan_set_level(im_volume_plan* p, int level, const double* ctrl, const double* alpha,
+                             size_t nc, double D, int psi_kind, im_basis basis, int precision) {
+  return guarded(p->ctx, [&](Context& c) {
+    if (level < 0 || level >= 8) throw InvalidArgument("level index out of range (0..7)");
+    auto& L = p->levels[level];
+    L.nc = nc;
+    L.D = D;
+    L.psi_kind = psi_kind;
+    L.tiles.reserve(6 * ctrl_padded(nc));
+    DBuf<double> stage;
+    stage.reserve(6 * std::max<size_t>(nc, 1));
+    if (nc) {
+      IMB_CHECK(cudaMemcpy(stage.p, ctrl, nc * 24, cudaMemcpyHostToDevice));
+      IMB_CHECK(cudaMemcpy(stage.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice));
+    }
+    pack_controls_aos(c, stage.p, stage.p + 3 * nc, nc,
+                      precision == IM_EXACT ? 1.0 : 1.0 / basis.support_radius, L.tiles.p);
+    IMB_CHECK(cudaStreamSynchronize(c.stream));
+    p->n_levels = std::max(p->n_levels, level + 1);
+  });
+}
+
+// Runs `steps` volume-update steps (every level: compaction of d < D_l, then
+// the update accumulated into the resident field).  Each step is bracketed
+// by CUDA events on the context stream; with flush_l2 a 256 MiB write evicts
+// L2 before each step, outside the timed brackets.  stats (10 doubles):
+//   [0] sum of step times (ms)   [1] sum of volume-kernel times (ms)
+//   [2] volume-kernel launches    [3] kernels launched per step
+//   [4..7] active count of levels 0..3 in the last step
+int im_volume_plan_run_steps(im_volume_plan* p, im_basis basis, int precision, int steps,
+                             int flush_l2, double* stats) {
+  return guarded(p->ctx, [&](Context& c) {
+    const size_t flush_bytes = size_t(256) << 20;
+    if (flush_l2) p->flush.reserve(flush_bytes);
+    cudaEvent_t e0, e1, k0, k1;
+    IMB_CHECK(cudaEventCreate(&e0));
+    IMB_CHECK(cudaEventCreate(&e1));
+    IMB_CHECK(cudaEventCreate(&k0));
+    IMB_CHECK(cudaEventCreate(&k1));
+    double total = 0.0, kern = 0.0, launches = 0.0, per_step = 0.0;
+    for (int s = 0; s < steps; ++s) {
+      if (flush_l2) IMB_CHECK(cudaMemsetAsync(p->flush.p, s & 0xff, flush_bytes, c.stream));
+      IMB_CHECK(cudaEventRecord(e0, c.stream));
+      per_step = 0.0;
+      for (int l = 0; l < p->n_levels; ++l) {
+        const auto& L = p->levels[l];
+        if (L.D <= 0.0) continue;
+        const size_t na = compact_active(c, p->dist.p, p->n, L.D, p->active.p);
+        per_step += 3;
+        if (l < 4) stats[4 + l] = (double)na;
+        VolumeArgs a;
+        a.x = p->nodes.x.p, a.y = p->nodes.y.p, a.z = p->nodes.z.p;
+        a.active = p->active.p;
+        a.n_active = na;
+        a.dist = p->dist.p;
+        a.D = L.D;
+        a.psi_kind = L.psi_kind;
+        a.tiles = L.tiles.p;
+        a.n_ctrl = L.nc;
+        a.R = basis.support_radius;
+        a.kind = basis.kind;
+        a.dim = p->dim;
+        a.precision = precision == IM_EXACT ? Precision::Exact : Precision::Fast64;
+        a.acc_x = p->field.x.p, a.acc_y = p->field.y.p, a.acc_z = p->field.z.p;
+        IMB_CHECK(cudaEventRecord(k0, c.stream));
+        launch_volume(c, a);
+        IMB_CHECK(cudaEventRecord(k1, c.stream));
+        IMB_CHECK(cudaEventSynchronize(k1));
+        float km = 0.f;
+        IMB_CHECK(cudaEventElapsedTime(&km, k0, k1));
+        kern += km;
+        launches += na ? 1 : 0;
+        per_step += na ? 1 : 0;
+      }
+      IMB_CHECK(cudaEventRecord(e1, c.stream));
+      IMB_CHECK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      IMB_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+      total += ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(k0);
+    cudaEventDestroy(k1);
+    stats[0] = total;
+    stats[1] = kern;
+    stats[2] = launches;
+    stats[3] = per_step;
+  });
+}
+
+// Exact count of in-support pairs (eta < 1, the reference's phi != 0 test
+// up to rounding at eta == 1) of one plan level over its active set, for the
+// algorithmic-flop roofline (22 flops in support, 10 out, 3-D; 17 / 7 in 2-D).
+int im_volume_plan_count_support(im_volume_plan* p, int level, im_basis basis,
+                                 unsigned long long* in_support, unsigned long long* total) {
+  return guarded(p->ctx, [&](Context& c) {
+    const auto& L = p->levels[level];
+    const size_t na = compact_active(c, p->dist.p, p->n, L.D, p->active.p);
+    *total = (unsigned long long)na * L.nc;
+    *in_support = count_support_pairs(c, p->nodes, p->active.p, na, L.tiles.p, L.nc,
+                                      1.0 / basis.support_radius);
   });
 }
 

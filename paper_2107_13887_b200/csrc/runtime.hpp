@@ -168,6 +168,11 @@ void launch_volume(Context& ctx, const VolumeArgs& a);
 // ascending node ids to d_out and returns the count (synchronises).
 size_t compact_active(Context& ctx, const double* d_dist, size_t n, double D, uint32_t* d_out);
 
+// Number of (active node, control) pairs with |r_v - r_c| < R (fast path
+// arithmetic, tiles packed with scale 1/R).
+unsigned long long count_support_pairs(Context& ctx, const DPoints& nodes, const uint32_t* active,
+                                       size_t n, const double* tiles, size_t nc, double inv_R);
+
 // Exclusive scan of n u32 counts into n+1 u64 offsets (out[n] = total).
 void scan_u32_to_u64(Context& ctx, const unsigned int* in, size_t n, unsigned long long* out);
 

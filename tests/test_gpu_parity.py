@@ -1,0 +1,322 @@
+"""Parity of the CUDA product (through its C-ABI) with the CPU oracle.
+
+Bar (north star): greedy control indices and the active volume set are
+bit-exact; displacements agree to 1e-10 relative in FP64.  The product's
+EXACT mode reproduces the reference's operation order, so most checks below
+are bit-for-bit (np.array_equal); the FP64 fast path is held to 1e-10
+relative to max |reference|.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2107_13887_b200 import capi, workloads as W
+
+pytestmark = pytest.mark.gpu
+FAST_TOL = 1e-10  # north-star FP64 tolerance, relative to max |reference|
+
+
+def rel_err(a, b):
+    scale = np.abs(b).max() if b.size else 0.0
+    return np.abs(a - b).max() / scale if scale > 0 else np.abs(a - b).max()
+
+
+def circle(n):
+    t = 2 * np.pi * np.arange(n) / n
+    return (np.stack([np.cos(t), np.sin(t), 0 * t], 1),
+            np.stack([0 * t, 0.1 * np.sin(2 * t) + 0.05 * np.cos(t), 0 * t], 1))
+
+
+# ---- rbf -------------------------------------------------------------------------
+@pytest.mark.parametrize("kind", ["c0", "c2", "c4", "c6"])
+@pytest.mark.parametrize("R", [0.05, 0.3, 1.0, 1e6])
+def test_eval_interpolant(gpu, oracle, kind, R):
+    rng = np.random.default_rng(1)
+    ctrl, alpha = rng.random((300, 3)), rng.standard_normal((300, 3))
+    q = rng.random((3000, 3)) * 2 - 0.5
+    ref = oracle.eval_interpolant(ctrl, alpha, kind, R, q)
+    assert np.array_equal(gpu.eval_interpolant(ctrl, alpha, kind, R, q, capi.EXACT), ref)
+    assert rel_err(gpu.eval_interpolant(ctrl, alpha, kind, R, q, capi.FP64), ref) < FAST_TOL
+
+
+def test_eval_interpolant_edge_cases(gpu, oracle):
+    # empty control set -> exact zeros; a query on a control -> phi(0) = 1
+    q = np.array([[0.5, 0.5, 0.0], [0.0, 0.0, 0.0]])
+    assert (gpu.eval_interpolant(np.zeros((0, 3)), np.zeros((0, 3)), "c2", 1.0, q) == 0).all()
+    c = np.array([[0.0, 0.0, 0.0]])
+    a = np.array([[0.3, -0.2, 0.1]])
+    out = gpu.eval_interpolant(c, a, "c2", 1.0, q, capi.FP64)
+    assert np.array_equal(out[1], a[0])
+    assert rel_err(out, oracle.eval_interpolant(c, a, "c2", 1.0, q)) < FAST_TOL
+
+
+def test_solve_weights_golden(gpu, golden):
+    g = golden
+    assert np.array_equal(gpu.solve_weights(g["sw_pts"], g["sw_disp"], "c2", 0.9), g["sw_alpha"])
+
+
+@pytest.mark.parametrize("kind", ["c0", "c2", "c4", "c6"])
+def test_solve_weights(gpu, oracle, kind):
+    rng = np.random.default_rng(7)
+    p, d = rng.random((150, 3)), rng.standard_normal((150, 3))
+    assert np.array_equal(gpu.solve_weights(p, d, kind, 0.5), oracle.solve_weights(p, d, kind, 0.5))
+
+
+def test_solve_weights_edge_cases(gpu):
+    assert gpu.solve_weights(np.zeros((0, 3)), np.zeros((0, 3))).shape == (0, 3)
+    z = gpu.solve_weights([[0, 0, 0], [0.25, 0, 0]], np.zeros((2, 3)), "c2", 1.0)
+    assert (z == 0).all()
+    with pytest.raises(capi.SolveError, match="points 0 and 1"):
+        gpu.solve_weights([[0, 0, 0], [1e-18, 0, 0]], [[1, 0, 0], [2, 0, 0]], "c2", 1.0)
+    with pytest.raises(ValueError):
+        gpu.solve_weights([[0, 0, 0]], [[1, 0, 0], [2, 0, 0]])
+
+
+# ---- greedy ---------------------------------------------------------------------------
+def test_greedy_golden(gpu, golden):
+    g = golden
+    for t in range(4):
+        r = gpu.greedy_level(g[f"greedy{t}_pos"], g[f"greedy{t}_tgt"], 0.05, 5000, "c2", 1.5)
+        assert np.array_equal(r.control_indices, g[f"greedy{t}_idx"])
+        assert np.array_equal(r.alpha, g[f"greedy{t}_alpha"])
+        assert np.array_equal(r.record_error, g[f"greedy{t}_err"])
+        assert np.array_equal(r.residual, g[f"greedy{t}_res"])
+        assert list(r.record_points) == list(range(1, len(r.record_error) + 1))
+
+
+def test_multilevel_golden(gpu, golden):
+    g = golden
+    m = gpu.run_multilevel(g["circle_pos"], g["circle_tgt"], 0.3, 3, 5000, "c2", 3.0)
+    assert len(m.levels) == int(g["circle_nlevels"])
+    for l, lv in enumerate(m.levels):
+        assert np.array_equal(lv.control_indices, g[f"circle_l{l}_idx"])
+        assert np.array_equal(lv.alpha, g[f"circle_l{l}_alpha"])
+    assert np.array_equal(m.final_residual, g["circle_final"])
+
+
+def test_greedy_kats(gpu):
+    r = gpu.greedy_level([[0, 0, 0], [0.5, 0, 0], [1, 0, 0]], [[0, 0, 0], [0, 1, 0], [0, 0, 0]],
+                         0.1, 5000, "c2", 2.0)
+    assert list(r.control_indices[:2]) == [0, 1] and r.achieved_error < 0.1
+    z = gpu.greedy_level([[0, 0, 0], [1, 0, 0], [2, 0, 0]], np.zeros((3, 3)), 0.1, 5000, "c2", 2.0)
+    assert list(z.control_indices) == [0] and z.achieved_error == 0.0 and not z.cap_hit
+    pos, tgt = circle(40)
+    c = gpu.greedy_level(pos, tgt, 1e-6, 3, "c2", 4.0)
+    assert len(c.control_indices) == 3 and c.cap_hit
+    with pytest.raises(capi.SolveError, match="surface nodes 0 and 1 are too close"):
+        gpu.greedy_level([[0, 0, 0], [0, 0, 0], [1, 0, 0]], [[0, 1, 0], [0, 2, 0], [0, 0, 0]],
+                         1e-9, 5000, "c2", 2.0)
+
+
+def test_greedy_invalid_arguments(gpu):
+    pos, tgt = circle(10)
+    for tol in (0.0, 1.0, -1.0):
+        with pytest.raises(ValueError, match="tolerance"):
+            gpu.greedy_level(pos, tgt, tol)
+    with pytest.raises(ValueError, match="empty"):
+        gpu.greedy_level(np.zeros((0, 3)), np.zeros((0, 3)), 0.1)
+    bad = tgt.copy()
+    bad[3, 1] = np.nan
+    with pytest.raises(ValueError, match="not finite"):
+        gpu.greedy_level(pos, bad, 0.1)
+    with pytest.raises(ValueError, match="support radius"):
+        gpu.greedy_level(pos, tgt, 0.1, R=0.0)
+
+
+@pytest.mark.parametrize("seed,dim,R,tol", [(3, 2, 0.3, 0.01), (4, 3, 0.5, 0.02), (5, 3, 2.0, 0.05),
+                                            (6, 2, 0.15, 0.003)])
+def test_multilevel_random(gpu, oracle, seed, dim, R, tol):
+    rng = np.random.default_rng(seed)
+    pos = rng.random((400, 3))
+    tgt = rng.standard_normal((400, 3)) * 0.01
+    if dim == 2:
+        pos[:, 2] = 0
+        tgt[:, 2] = 0
+    a = gpu.run_multilevel(pos, tgt, tol, 3, 5000, "c2", R)
+    b = oracle.run_multilevel(pos, tgt, tol, 3, 5000, "c2", R)
+    assert len(a.levels) == len(b.levels)
+    for la, lb in zip(a.levels, b.levels):
+        assert np.array_equal(la.control_indices, lb.control_indices)
+        assert np.array_equal(la.alpha, lb.alpha)
+        assert np.array_equal(la.record_error, lb.record_error)
+        assert la.cap_hit == lb.cap_hit and la.achieved_error == lb.achieved_error
+    assert np.array_equal(a.final_residual, b.final_residual)
+
+
+def test_greedy_symmetric_ties(gpu, oracle):
+    """Mirror-symmetric airfoil + LE bump: residual norms of mirror nodes tie
+    up to rounding at nearly every step; indices must still match."""
+    w = W.cfg1(0.5)
+    pos = w.nodes[w.surface]
+    a = gpu.run_multilevel(pos, w.displacement, w.tol, w.levels, w.cap, w.kind, w.R)
+    b = oracle.run_multilevel(pos, w.displacement, w.tol, w.levels, w.cap, w.kind, w.R)
+    for la, lb in zip(a.levels, b.levels):
+        assert np.array_equal(la.control_indices, lb.control_indices)
+        assert np.array_equal(la.alpha, lb.alpha)
+
+
+# ---- wall distance ------------------------------------------------------------------
+def test_wall_distance_golden(gpu, golden):
+    g = golden
+    assert np.array_equal(gpu.build_distance_index(g["wd_nodes"], 3, np.arange(1000)), g["wd_dist"])
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_wall_distance_random(gpu, oracle, dim):
+    rng = np.random.default_rng(11 + dim)
+    nodes = rng.uniform(-2, 2, (30000, 3))
+    if dim == 2:
+        nodes[:, 2] = 0
+    surf = rng.choice(30000, 700, replace=False)
+    assert np.array_equal(gpu.build_distance_index(nodes, dim, surf),
+                          oracle.build_distance_index(nodes, dim, surf))
+
+
+def test_wall_distance_airfoil(gpu, oracle):
+    w = W.cfg1(0.5)
+    assert np.array_equal(gpu.build_distance_index(w.nodes, 2, w.surface),
+                          oracle.build_distance_index(w.nodes, 2, w.surface))
+
+
+def test_wall_distance_edge_cases(gpu):
+    d = gpu.build_distance_index([[0, 0, 0], [1, 0, 0], [0.5, 1, 0], [4, 0, 0]], 2, [0, 1])
+    assert d[0] == 0 and d[1] == 0 and d[2] == pytest.approx(math.sqrt(1.25), rel=1e-15)
+    assert d[3] == 3.0
+    with pytest.raises(ValueError, match="empty patch"):
+        gpu.build_distance_index([[0, 0, 0]], 2, [])
+    # one-point patch, collinear and coincident points
+    d = gpu.build_distance_index([[1, 1, 1], [1, 1, 1], [2, 1, 1]], 3, [0])
+    assert list(d) == [0.0, 0.0, 1.0]
+
+
+# ---- volume update --------------------------------------------------------------------
+@pytest.mark.parametrize("psi", [0, 1])
+def test_update_volume_golden(gpu, golden, psi):
+    g = golden
+    i, v = gpu.update_volume(g["wd_nodes"], g["wd_dist"], g["wd_nodes"][:40], g["uv_alpha"], 0.35,
+                             psi, "c2", 0.5, capi.EXACT)
+    assert np.array_equal(i, g[f"uv{psi}_idx"]) and np.array_equal(v, g[f"uv{psi}_val"])
+    i, v = gpu.update_volume(g["wd_nodes"], g["wd_dist"], g["wd_nodes"][:40], g["uv_alpha"], 0.35,
+                             psi, "c2", 0.5, capi.FP64)
+    assert np.array_equal(i, g[f"uv{psi}_idx"]) and rel_err(v, g[f"uv{psi}_val"]) < FAST_TOL
+
+
+@pytest.mark.parametrize("R,D", [(0.05, 0.1), (0.2, 0.5), (1.0, math.inf), (math.inf, 0.5)])
+def test_update_volume_raw(gpu, oracle, R, D):
+    """Raw kernel sweep shapes (BASELINE cfg5) at oracle-sized scale."""
+    raw = W.raw(500, 40000, R if math.isfinite(R) else 1e300, D, n_wall=800)
+    nodes = np.vstack([raw["vol"], raw["wall"]])
+    surface = np.arange(len(raw["vol"]), len(nodes))
+    d = gpu.build_distance_index(nodes, 3, surface)
+    Rv = raw["R"]
+    i0, v0 = oracle.update_volume(nodes, d, raw["ctrl"], raw["alpha"], D, 0, "c2", Rv)
+    i1, v1 = gpu.update_volume(nodes, d, raw["ctrl"], raw["alpha"], D, 0, "c2", Rv, capi.EXACT)
+    assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
+    i2, v2 = gpu.update_volume(nodes, d, raw["ctrl"], raw["alpha"], D, 0, "c2", Rv, capi.FP64)
+    assert np.array_equal(i0, i2) and rel_err(v2, v0) < FAST_TOL
+
+
+def test_update_volume_edge_cases(gpu):
+    nodes = np.array([[0, 0, 0], [0, 0.05, 0], [0, 0.2, 0], [0, 5, 0]], float)
+    d = gpu.build_distance_index(nodes, 2, [0])
+    i, v = gpu.update_volume(nodes, d, [[0, 0, 0]], [[0, 0.7, 0]], 0.1, 0, "c2", 2.0, capi.EXACT)
+    assert list(i) == [0, 1] and (v[0] == [0, 0.7, 0]).all()
+    i, v = gpu.update_volume(nodes, d, [[0, 0, 0]], [[0, 0.7, 0]], 0.0, 0, "c2", 2.0)
+    assert len(i) == 0  # D = 0: no volume work (wall_distance.cpp:54)
+    i, v = gpu.update_volume(nodes, d, np.zeros((0, 3)), np.zeros((0, 3)), 1.0, 0, "c2", 2.0)
+    assert list(i) == [0, 1, 2] and (v == 0).all()
+    with pytest.raises(ValueError):
+        gpu.update_volume(nodes, d[:2], [[0, 0, 0]], [[0, 0.7, 0]], 0.1)
+
+
+def test_update_volume_linearity_full_size(gpu):
+    """Size-independent property at BASELINE cfg2 scale (1M nodes): the update
+    is linear in alpha, and the active set is exactly {d < D}."""
+    w = W.cfg2()
+    d = gpu.build_distance_index(w.nodes, 2, w.surface)
+    rng = np.random.default_rng(2)
+    ctrl = w.nodes[w.surface][::40]
+    a1, a2 = rng.standard_normal((len(ctrl), 3)) * 0.01, rng.standard_normal((len(ctrl), 3)) * 0.01
+    a1[:, 2] = a2[:, 2] = 0
+    i1, v1 = gpu.update_volume(w.nodes, d, ctrl, a1, w.D, 0, "c2", w.R)
+    i2, v2 = gpu.update_volume(w.nodes, d, ctrl, a2, w.D, 0, "c2", w.R)
+    i3, v3 = gpu.update_volume(w.nodes, d, ctrl, a1 + a2, w.D, 0, "c2", w.R)
+    assert np.array_equal(i1, np.flatnonzero(d < w.D)) and np.array_equal(i1, i3)
+    assert rel_err(v3, v1 + v2) < 1e-12
+
+
+# ---- deform ------------------------------------------------------------------------------
+def test_deform_golden(gpu, golden):
+    g = golden
+    r = gpu.deform(g["cfg1s_nodes"], 2, g["cfg1s_surface"], g["cfg1s_disp"], (), 1e-3, 2, 5000,
+                   "c2", 0.5, 5.0, -1.0, 0, capi.EXACT)
+    assert np.array_equal(r["nodes"], g["cfg1s_deformed"])
+    assert np.array_equal(r["touched"], g["cfg1s_touched"])
+    f = gpu.deform(g["cfg1s_nodes"], 2, g["cfg1s_surface"], g["cfg1s_disp"], (), 1e-3, 2, 5000,
+                   "c2", 0.5, 5.0, -1.0, 0, capi.FP64)
+    base = g["cfg1s_nodes"]
+    assert rel_err(f["nodes"] - base, g["cfg1s_deformed"] - base) < FAST_TOL
+
+
+def test_deform_against_reference(gpu, ref):
+    w = W.cfg1(0.6)
+    a = gpu.deform(w.nodes, 2, w.surface, w.displacement, (), w.tol, w.levels, w.cap, w.kind, w.R,
+                   5.0, -1.0, 0, capi.EXACT)
+    b = ref.deform(w.nodes, 2, w.surface, w.displacement, (), w.tol, w.levels, w.cap, w.kind, w.R,
+                   5.0)
+    assert np.array_equal(a["nodes"], b["nodes"])
+    assert np.array_equal(a["touched"], b["touched"]) and np.array_equal(a["points"], b["points"])
+    assert a["surface_max_error"] == b["surface_max_error"]
+    assert a["surface_mean_error"] == b["surface_mean_error"]
+
+
+def test_deform_pinned_and_far_nodes(gpu, ref):
+    """Pinned markers never move (test_pipeline.cpp:61-77); nodes beyond every
+    support distance stay bitwise unmoved (:79-100)."""
+    w = W.cfg1(0.3)
+    ring = int(w.meta["ring"])
+    outer = np.arange(len(w.nodes) - len(w.surface) - ring, len(w.nodes) - len(w.surface))
+    try:
+        b = ref.deform(w.nodes, 2, w.surface, w.displacement, outer, 0.1, 3, 5000, "c2", 30.0, 1e4)
+    except Exception as e:  # ill-conditioned: the product must fail identically
+        with pytest.raises(capi.SolveError) as g:
+            gpu.deform(w.nodes, 2, w.surface, w.displacement, outer, 0.1, 3, 5000, "c2", 30.0, 1e4,
+                       -1.0, 0, capi.EXACT)
+        assert str(g.value) == str(e)
+    else:
+        a = gpu.deform(w.nodes, 2, w.surface, w.displacement, outer, 0.1, 3, 5000, "c2", 30.0, 1e4,
+                       -1.0, 0, capi.EXACT)
+        assert np.array_equal(a["nodes"][outer], w.nodes[outer])
+        assert np.array_equal(a["nodes"], b["nodes"])
+    c = gpu.deform(w.nodes, 2, w.surface, w.displacement, (), 0.1, 3, 5000, "c2", 2.0, 5.0, -1.0,
+                   0, capi.FP64)
+    d = gpu.build_distance_index(w.nodes, 2, w.surface)
+    far = d >= c["support"].max()
+    assert far.any() and np.array_equal(c["nodes"][far], w.nodes[far])
+
+
+def test_deform_zero_field_identity(gpu):
+    w = W.cfg1(0.3)
+    r = gpu.deform(w.nodes, 2, w.surface, np.zeros_like(w.displacement), (), 0.1, 5, 5000, "c2",
+                   2.0, 5.0)
+    assert np.array_equal(r["nodes"], w.nodes) and len(r["points"]) == 1
+    assert r["surface_max_error"] == 0.0
+
+
+def test_deform_absolute_support_and_c2_taper(gpu, oracle):
+    """The configs' additive extensions: absolute D and the Wendland-C2 taper,
+    checked level by level against the oracle's update_volume."""
+    w = W.cfg1(0.4)
+    a = gpu.deform(w.nodes, 2, w.surface, w.displacement, (), w.tol, w.levels, w.cap, w.kind, w.R,
+                   5.0, w.D, 1, capi.EXACT)
+    pos = w.nodes[w.surface]
+    m = oracle.run_multilevel(pos, w.displacement, w.tol, w.levels, w.cap, w.kind, w.R)
+    d = oracle.build_distance_index(w.nodes, 2, w.surface)
+    expect = w.nodes.copy()
+    for lv in m.levels:
+        i, v = oracle.update_volume(w.nodes, d, pos[lv.control_indices], lv.alpha, w.D, 1, "c2",
+                                    w.R)
+        expect[i] += v
+    assert np.array_equal(a["nodes"], expect)
+    assert list(a["touched"]) == [int((d < w.D).sum())] * len(m.levels)
