@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kInsertThreads) k_insert(GView g) {
   const size_t cap = g.cap;
   double* rr = sh;                   // [cap]
   double* ring = sh + cap;           // [2][cap]
-  double2* dgs = reinterpret_cast<double2*>(sh + 3 * cap);  // [cap] if staged
+  double2* dgs = reinterpret_cast<double2*>(sh + ((3 * cap + 1) & ~size_t(1)));  // [cap], 16B-aligned
   const int tid = threadIdx.x;
   const int k = st.nc;
   const int node = st.next;
@@ -224,42 +224,60 @@ __device__ __forceinline__ void bw_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// Per block of (up to kBwBlock) elements of a column of L^T:
-//   phase A (32 lanes): P[a][e] = L_ji * x_j[a] for the three axes, from the
-//            TMA-streamed L block and x in shared memory;
-//   phase B (lanes 0..2): lane a runs the dependent chain s -= P[a][e] of its
-//            axis, a pure LDS + DSUB loop that runs at the 8-cycle DSUB
-//            latency (tools/chain_probe.cu) -- the products are off the chain.
-// x_i = s / L_ii closes each column.  Columns stream into a ring of
-// shared-memory blocks by 1-D TMA bulk copies (mbarrier completion),
-// kBwRing blocks ahead of the chain.
+// Two warps, producer / consumer, per block of (up to kBwBlock) elements of
+// a column of L^T:
+//   warp 1 (producer, 32 lanes): P[a][e] = L_ji * x_j[a] for the three axes,
+//            from the TMA-streamed L block and x in shared memory, into one
+//            of two product buffers;
+//   warp 0 (consumer, lanes 0..2): lane a runs the dependent chain
+//            s -= P[a][e] of its axis -- a pure LDS + DSUB loop at the 8-cycle
+//            DSUB latency -- and closes each column with x_i = s / L_ii.
+// The column head (j = i+1) needs x_{i+1}, solved by the consumer at the end
+// of the previous block, so the producer leaves it at +0 and passes its L
+// value; the consumer applies it first, from registers, keeping the
+// reference's ascending-j order (rbf.cpp:116-118).  Every other x_j a block
+// needs was solved >= 2 blocks earlier, which the empty-buffer handshake
+// orders before the producer reads it.  mbarrier phases: full[b] (producer
+// -> consumer), empty[b] (consumer -> producer), ring[r] (TMA -> producer).
 struct BwBlock {
   int i, e0;  // column i, elements e0.. of rows j = i+1+e
 };
 
+__device__ __forceinline__ void bw_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+
+constexpr int kBwPad = kBwBlock + 32;
+
 template <bool XS_SMEM>
-__global__ void __launch_bounds__(32) k_backward_t(GView g) {
+__global__ void __launch_bounds__(64) k_backward_t(GView g) {
   const GState& st = *g.st;
   if (st.status != 0) return;
   extern __shared__ __align__(16) double sh[];
-  const int lane = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = st.nc;
   const size_t cap = g.cap;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sh);        // [kBwRing]
-  double* ring = sh + kBwRing;                            // [kBwRing][kBwBlock+2]
-  double* P = ring + kBwRing * (kBwBlock + 2);            // [3][kBwBlock + 32]
+  uint64_t* ringbar = reinterpret_cast<uint64_t*>(sh);  // [kBwRing]
+  uint64_t* full = ringbar + kBwRing;                   // [2]
+  uint64_t* empty = full + 2;                           // [2]
+  double* headL = sh + kBwRing + 4;                     // [2] (+2 pad)
+  double* ring = sh + kBwRing + 8;                      // [kBwRing][kBwBlock+2]
+  double* P = ring + kBwRing * (kBwBlock + 2);          // [2][3][kBwPad]
   // comp: X[cap] | Y[cap] | Z[cap] | D[cap]; X/Y/Z start as y and become x
   // once solved (s = x[i] at rbf.cpp:115 reads its own slot)
-  double* comp = XS_SMEM ? P + 3 * (kBwBlock + 32) : g.xs_global;
+  double* comp = XS_SMEM ? P + 6 * kBwPad : g.xs_global;
   if (n == 0) return;
-  for (int j = lane; j < n; j += 32) {
+  for (int j = tid; j < n; j += 64) {
     comp[j] = g.yx[j], comp[cap + j] = g.yy[j], comp[2 * cap + j] = g.yz[j];
     comp[3 * cap + j] = g.diag[j].x;
   }
-  if (lane == 0)
-    for (int r = 0; r < kBwRing; ++r) bw_mbar_init(&bar[r]);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncwarp();
+  if (tid == 0) {
+    for (int r = 0; r < kBwRing + 4; ++r) bw_mbar_init(&ringbar[r]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   auto next = [&](BwBlock b) -> BwBlock {
     if (b.e0 + kBwBlock < n - 1 - b.i) return {b.i, b.e0 + kBwBlock};
     return {b.i - 1, 0};
@@ -271,55 +289,66 @@ __global__ void __launch_bounds__(32) k_backward_t(GView g) {
     cnt = min(kBwBlock, n - 1 - b.i - b.e0);
     return reinterpret_cast<const double*>(al);
   };
-  auto issue = [&](BwBlock b, int slot) {
-    if (lane != 0 || b.i < 0) return;
-    int off, cnt;
-    const double* al = src_of(b, off, cnt);
-    const uint32_t bytes = (uint32_t)(((off + cnt) * 8 + 15) & ~15);
-    bw_bulk(ring + slot * (kBwBlock + 2), al, bytes, &bar[slot]);
-  };
   const double* dd = comp + 3 * cap;
-  if (lane < 3) {  // x_{n-1} = y_{n-1} / L_{n-1,n-1}
-    double* cx = comp + (size_t)lane * cap;
-    cx[n - 1] = exact::div_rcp(cx[n - 1], exact::make_recip(dd[n - 1]));
-  }
-  __syncwarp();
-  BwBlock cur{n - 2, 0}, ahead = cur;
-  for (int r = 0; r < kBwRing; ++r) {
-    issue(ahead, r);
-    ahead = next(ahead);
-  }
-  double s = 0.0;
-  for (int t = 0; cur.i >= 0; ++t) {
-    const int slot = t % kBwRing;
-    const int i = cur.i;
-    int off, cnt;
-    src_of(cur, off, cnt);
-    bw_wait(&bar[slot], (uint32_t)((t / kBwRing) & 1));
-    // phase A: products for the three axes
-    {
+  if (warp == 1) {
+    // ---------------- producer ----------------
+    auto issue = [&](BwBlock b, int slot) {
+      if (lane != 0 || b.i < 0) return;
+      int off, cnt;
+      const double* al = src_of(b, off, cnt);
+      const uint32_t bytes = (uint32_t)(((off + cnt) * 8 + 15) & ~15);
+      bw_bulk(ring + slot * (kBwBlock + 2), al, bytes, &ringbar[slot]);
+    };
+    BwBlock cur{n - 2, 0}, ahead = cur;
+    for (int r = 0; r < kBwRing; ++r) {
+      issue(ahead, r);
+      ahead = next(ahead);
+    }
+    for (int t = 0; cur.i >= 0; ++t) {
+      const int slot = t % kBwRing, pb = t & 1;
+      int off, cnt;
+      src_of(cur, off, cnt);
+      bw_wait(&ringbar[slot], (uint32_t)((t / kBwRing) & 1));
+      bw_wait(&empty[pb], (uint32_t)(((t >> 1) & 1) ^ 1));
       const double* lb = ring + slot * (kBwBlock + 2) + off;
-      const int j0 = i + 1 + cur.e0;
+      double* pp = P + pb * 3 * kBwPad;
+      const int j0 = cur.i + 1 + cur.e0;
+      const bool head = cur.e0 == 0;
       for (int e = lane; e < cnt; e += 32) {
         const double l = lb[e];
-        P[e] = exact::mul(l, comp[j0 + e]);
-        P[(kBwBlock + 32) + e] = exact::mul(l, comp[cap + j0 + e]);
-        P[2 * (kBwBlock + 32) + e] = exact::mul(l, comp[2 * cap + j0 + e]);
+        if (head && e == 0) {
+          headL[pb] = l;
+          pp[0] = pp[kBwPad] = pp[2 * kBwPad] = 0.0;  // s - (+0) == s
+        } else {
+          pp[e] = exact::mul(l, comp[j0 + e]);
+          pp[kBwPad + e] = exact::mul(l, comp[cap + j0 + e]);
+          pp[2 * kBwPad + e] = exact::mul(l, comp[2 * cap + j0 + e]);
+        }
       }
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bw_arrive(&full[pb]);
+      }
+      issue(ahead, slot);  // refill the slot just consumed
+      ahead = next(ahead);
+      cur = next(cur);
     }
-    __syncwarp();
-    if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    issue(ahead, slot);  // refill the slot just consumed
-    ahead = next(ahead);
-    const BwBlock nx = next(cur);
-    // phase B: the dependent chains, rbf.cpp:116-118 in ascending j
-    if (lane < 3) {
-      double* cx = comp + (size_t)lane * cap;
-      const double* pa = P + lane * (kBwBlock + 32);
-      if (cur.e0 == 0) s = cx[i];
-      // ping-pong register sets: the loads of one 16-group run under the
-      // chain of the other (no rotation moves).  P is zero-padded past cnt
-      // below, so whole groups are always safe to load.
+  } else if (lane < 3) {
+    // ---------------- consumer ----------------
+    double* cx = comp + (size_t)lane * cap;
+    cx[n - 1] = exact::div_rcp(cx[n - 1], exact::make_recip(dd[n - 1]));  // x_{n-1}
+    BwBlock cur{n - 2, 0};
+    double s = 0.0;
+    for (int t = 0; cur.i >= 0; ++t) {
+      const int pb = t & 1, i = cur.i;
+      int off, cnt;
+      src_of(cur, off, cnt);
+      bw_wait(&full[pb], (uint32_t)((t >> 1) & 1));
+      const double* pa = P + pb * 3 * kBwPad + lane * kBwPad;
+      if (cur.e0 == 0) s = exact::sub(cx[i], exact::mul(headL[pb], cx[i + 1]));
+      // ping-pong register sets: loads of one 16-group run under the chain of
+      // the other (no rotation moves); pa is padded so whole groups are safe.
       double ra[16], rb[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) ra[u] = pa[u];
@@ -335,12 +364,15 @@ __global__ void __launch_bounds__(32) k_backward_t(GView g) {
         for (int u = 0; u < 16; ++u) s = exact::sub(s, rb[u]);
       }
       for (; e < cnt; ++e) s = exact::sub(s, pa[e]);
+      const BwBlock nx = next(cur);
       if (nx.i != i) cx[i] = exact::div_rcp(s, exact::make_recip(dd[i]));  // x_i = s / L_ii
+      __syncwarp(0x7u);
+      if (lane == 0) bw_arrive(&empty[pb]);
+      cur = nx;
     }
-    __syncwarp();
-    cur = nx;
   }
-  for (int i = lane; i < n; i += 32) g.ax[i] = comp[i], g.ay[i] = comp[cap + i], g.az[i] = comp[2 * cap + i];
+  __syncthreads();
+  for (int i = tid; i < n; i += 64) g.ax[i] = comp[i], g.ay[i] = comp[cap + i], g.az[i] = comp[2 * cap + i];
 }
 
 // ---------------------------------------------------------------------------
@@ -479,9 +511,9 @@ GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap
   st_.reserve(1);
   IMB_CHECK(cudaMallocHost(&hst_, sizeof(GState)));
   // x workspace of the backward chain: shared memory when it fits
-  const size_t head = (8 + 8 * (512 + 2) + 3 * (512 + 32)) * 8;  // mbarriers + L ring + products
+  const size_t head = (8 + 8 + 8 * (512 + 2) + 6 * (512 + 32)) * 8;  // barriers, L ring, products
   const size_t xs_bytes = (size_t)cap * 32 + head;
-  if (xs_bytes <= 200 * 1024) {
+  if (xs_bytes <= 227 * 1024) {
     bw_smem_ = xs_bytes;
   } else {
     xs_.reserve((size_t)cap * 4);
@@ -493,7 +525,7 @@ GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap
                                  (int)std::max<size_t>(bw_smem_, 48 * 1024)));
   // k_insert: rr + ring[2] (+ dg staging, which also makes room for y)
   ins_smem_ = (size_t)cap * 24;
-  if ((size_t)cap * 40 <= 210 * 1024) ins_smem_ = (size_t)cap * 40, ins_dg_smem_ = 1;
+  if ((size_t)cap * 40 + 16 <= 210 * 1024) ins_smem_ = (size_t)cap * 40 + 16, ins_dg_smem_ = 1;
   ins_y_smem_ = ins_dg_smem_;
   IMB_CHECK(cudaFuncSetAttribute(k_insert, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)std::max<size_t>(ins_smem_, 48 * 1024)));
@@ -561,9 +593,9 @@ const GState& GreedyEngine::poll() {
 
 void GreedyEngine::launch_backward(const GView& g) {
   if (xs_.p)
-    k_backward_t<false><<<1, 32, bw_smem_, ctx_.stream>>>(g);
+    k_backward_t<false><<<1, 64, bw_smem_, ctx_.stream>>>(g);
   else
-    k_backward_t<true><<<1, 32, bw_smem_, ctx_.stream>>>(g);
+    k_backward_t<true><<<1, 64, bw_smem_, ctx_.stream>>>(g);
 }
 
 void GreedyEngine::enqueue_step(bool sweep) {
