@@ -320,3 +320,23 @@ def test_deform_absolute_support_and_c2_taper(gpu, oracle):
         expect[i] += v
     assert np.array_equal(a["nodes"], expect)
     assert list(a["touched"]) == [int((d < w.D).sum())] * len(m.levels)
+
+
+def test_cfg2_full_selection(gpu):
+    """Full BASELINE cfg2 (10k mirror-symmetric surface points, cap 5000):
+    the device greedy selects exactly the reference's control points.  The
+    reference indices come from the unmodified reference run_multilevel
+    (tests/golden/make_cfg2_selection.py, ~27 min on one CPU core).  Levels
+    0-1 always; the capped 5000-point level 2 (~2 min on the device) with
+    IMB_FULL=1."""
+    import os
+
+    ref = np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg2_reference_selection.npz"))
+    w = W.cfg2()
+    pos = w.nodes[w.surface]
+    levels = 3 if os.environ.get("IMB_FULL") == "1" else 2
+    m = gpu.run_multilevel(pos, w.displacement, w.tol, levels, w.cap, w.kind, w.R)
+    assert len(m.levels) == levels
+    for l, lv in enumerate(m.levels):
+        assert np.array_equal(lv.control_indices, ref[f"idx{l}"]), f"level {l}"
+        assert lv.cap_hit == bool(ref["cap_hit"][l])
