@@ -275,16 +275,20 @@ int im_eval_interpolant(im_context* ctx, const double* ctrl, const double* alpha
     const size_t np = ctrl_padded(nc);
     DBuf<double> staging, tiles, dout;
     staging.reserve(6 * std::max<size_t>(nc, 1));
-    tiles.reserve(6 * np);
+    tiles.reserve(ctrl_tile_doubles(nc));
     dout.reserve(3 * nq);
     if (nc) {
       IMB_CHECK(cudaMemcpyAsync(staging.p, ctrl, nc * 24, cudaMemcpyHostToDevice, c.stream));
       IMB_CHECK(cudaMemcpyAsync(staging.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice, c.stream));
     }
     const bool exact = precision == IM_EXACT;
-    pack_controls_aos(c, staging.p, staging.p + 3 * nc, nc,
-                      exact ? 1.0 : 1.0 / basis.support_radius, tiles.p);
+    DBuf<double> boxes;
+    if (exact)
+      pack_controls_aos(c, staging.p, staging.p + 3 * nc, nc, 1.0, tiles.p);
+    else
+      pack_controls_host(c, ctrl, alpha, nc, 1.0 / basis.support_radius, true, tiles, boxes);
     VolumeArgs a;
+    a.tile_box = exact ? nullptr : boxes.p;
     a.x = q.x.p, a.y = q.y.p, a.z = q.z.p;
     a.n_active = nq;
     a.tiles = tiles.p;
@@ -412,16 +416,20 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     active.reserve(n_nodes);
     IMB_CHECK(cudaMemcpyAsync(dd.p, dist, n_nodes * 8, cudaMemcpyHostToDevice, c.stream));
     staging.reserve(6 * std::max<size_t>(nc, 1));
-    tiles.reserve(6 * ctrl_padded(nc));
+    tiles.reserve(ctrl_tile_doubles(nc));
     if (nc) {
       IMB_CHECK(cudaMemcpyAsync(staging.p, ctrl, nc * 24, cudaMemcpyHostToDevice, c.stream));
       IMB_CHECK(cudaMemcpyAsync(staging.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice, c.stream));
     }
     const bool exact = precision == IM_EXACT;
+    DBuf<double> boxes;
+    if (!exact)
+      pack_controls_host(c, ctrl, alpha, nc, 1.0 / basis.support_radius, true, tiles, boxes);
     EventTimer tm(c.stream);
-    pack_controls_aos(c, staging.p, staging.p + 3 * nc, nc,
-                      exact ? 1.0 : 1.0 / basis.support_radius, tiles.p);
+    if (exact) pack_controls_aos(c, staging.p, staging.p + 3 * nc, nc, 1.0, tiles.p);
     const size_t na = compact_active(c, dd.p, n_nodes, D, active.p);
+    DBuf<uint32_t> perm;
+    if (!exact) spatial_order(c, dn.x.p, dn.y.p, dn.z.p, active.p, na, basis.support_radius, perm);
     vals.reserve(3 * std::max<size_t>(na, 1));
     VolumeArgs a;
     a.x = dn.x.p, a.y = dn.y.p, a.z = dn.z.p;
@@ -437,6 +445,8 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     a.dim = 3;
     a.precision = exact ? Precision::Exact : Precision::Fast64;
     a.out_val = vals.p;
+    a.tile_box = exact ? nullptr : boxes.p;
+    a.perm = exact ? nullptr : perm.p;
     launch_volume(c, a);
     c.last_kernel_ms = tm.stop();
     std::vector<uint32_t> idx(na);

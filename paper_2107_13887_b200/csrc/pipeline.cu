@@ -108,6 +108,26 @@ __global__ void k_set_flags(unsigned char* f, const unsigned long long* idx, siz
   if (i < n) f[idx[i]] = 1;
 }
 
+__global__ void k_gather(const double* src, const uint32_t* order, size_t n, double* dst) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[order[i]];
+}
+
+__global__ void k_scatter_aos(const double* x, const double* y, const double* z,
+                              const uint32_t* order, size_t n, double* aos) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t o = order[i];
+  aos[3 * o] = x[i];
+  aos[3 * o + 1] = y[i];
+  aos[3 * o + 2] = z[i];
+}
+
+__global__ void k_scatter1(const double* src, const uint32_t* order, size_t n, double* dst) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[order[i]] = src[i];
+}
+
 __global__ void k_soa_to_aos(const double* x, const double* y, const double* z, size_t n,
                              double* aos) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -132,13 +152,19 @@ struct im_volume_plan {
   size_t nc = 0;
   // multi-level step (bench): per-level packed controls and support distance
   struct Level {
-    DBuf<double> tiles;
+    DBuf<double> tiles, boxes;
+    bool culled = false;
     size_t nc = 0;
     double D = 0.0;
     int psi_kind = 0;
   };
   Level levels[8];
   int n_levels = 0;
+  DBuf<uint32_t> perm;
+  // spatial layout: node k' of the resident arrays is original node order[k']
+  // (grid-cell order, so compacted active sets are spatially coherent)
+  DBuf<uint32_t> order;
+  bool reordered = false;
   DBuf<unsigned char> flush;
 };
 
@@ -270,7 +296,8 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
     const bool planar = dim == 2 && all_z_zero(nodes, n_nodes);
     DBuf<uint32_t> active;
     active.reserve(n_nodes);
-    DBuf<double> stage, tiles;
+    DBuf<double> stage, tiles, boxes;
+    DBuf<uint32_t> perm;
     Timer tm(c.stream);
     for (size_t l = 0; l < levels.size(); ++l) {
       const Lvl& lv = levels[l];
@@ -280,16 +307,21 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
         std::vector<double> cp(3 * nc);
         for (size_t i = 0; i < nc; ++i) std::memcpy(&cp[3 * i], &pos[3 * lv.idx[i]], 24);
         stage.reserve(6 * std::max<size_t>(nc, 1));
-        tiles.reserve(6 * ctrl_padded(nc));
+        tiles.reserve(ctrl_tile_doubles(nc));
         if (nc) {
           IMB_CHECK(cudaMemcpyAsync(stage.p, cp.data(), nc * 24, cudaMemcpyHostToDevice, c.stream));
           IMB_CHECK(cudaMemcpyAsync(stage.p + 3 * nc, lv.alpha.data(), nc * 24,
                                     cudaMemcpyHostToDevice, c.stream));
         }
         const bool exact = cfg->precision == IM_EXACT;
-        pack_controls_aos(c, stage.p, stage.p + 3 * nc, nc,
-                          exact ? 1.0 : 1.0 / g.basis.support_radius, tiles.p);
+        if (exact)
+          pack_controls_aos(c, stage.p, stage.p + 3 * nc, nc, 1.0, tiles.p);
+        else
+          pack_controls_host(c, cp.data(), lv.alpha.data(), nc, 1.0 / g.basis.support_radius, true,
+                             tiles, boxes);
         touched = compact_active(c, dist.p, n_nodes, Dl[l], active.p);
+        if (!exact)
+          spatial_order(c, dn.x.p, dn.y.p, dn.z.p, active.p, touched, g.basis.support_radius, perm);
         VolumeArgs a;
         a.x = dn.x.p, a.y = dn.y.p, a.z = dn.z.p;
         a.active = active.p;
@@ -298,6 +330,8 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
         a.D = Dl[l];
         a.psi_kind = cfg->psi_kind;
         a.tiles = tiles.p;
+        a.tile_box = exact ? nullptr : boxes.p;
+        a.perm = exact ? nullptr : perm.p;
         a.n_ctrl = nc;
         a.R = g.basis.support_radius;
         a.kind = g.basis.kind;
@@ -397,7 +431,7 @@ int im_volume_plan_set_controls(im_volume_plan* p, const double* ctrl, const dou
   return guarded(p->ctx, [&](Context& c) {
     p->nc = nc;
     p->ctrl_stage.reserve(6 * std::max<size_t>(nc, 1));
-    p->tiles.reserve(6 * ctrl_padded(nc));
+    p->tiles.reserve(ctrl_tile_doubles(nc));
     if (nc) {
       IMB_CHECK(cudaMemcpy(p->ctrl_stage.p, ctrl, nc * 24, cudaMemcpyHostToDevice));
       IMB_CHECK(cudaMemcpy(p->ctrl_stage.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice));
@@ -451,8 +485,12 @@ int im_volume_plan_download_field(im_volume_plan* p, double* out) {
   return guarded(p->ctx, [&](Context& c) {
     DBuf<double> aos;
     aos.reserve(3 * p->n);
-    k_soa_to_aos<<<(p->n + 255) / 256, 256, 0, c.stream>>>(p->field.x.p, p->field.y.p,
-                                                            p->field.z.p, p->n, aos.p);
+    if (p->reordered)
+      k_scatter_aos<<<(p->n + 255) / 256, 256, 0, c.stream>>>(p->field.x.p, p->field.y.p,
+                                                              p->field.z.p, p->order.p, p->n, aos.p);
+    else
+      k_soa_to_aos<<<(p->n + 255) / 256, 256, 0, c.stream>>>(p->field.x.p, p->field.y.p,
+                                                              p->field.z.p, p->n, aos.p);
     IMB_CHECK(cudaMemcpyAsync(out, aos.p, p->n * 24, cudaMemcpyDeviceToHost, c.stream));
     IMB_CHECK(cudaStreamSynchronize(c.stream));
   });
@@ -460,6 +498,14 @@ int im_volume_plan_download_field(im_volume_plan* p, double* out) {
 
 int im_volume_plan_distances(im_volume_plan* p, double* out) {
   return guarded(p->ctx, [&](Context& c) {
+    if (p->reordered) {
+      DBuf<double> tmp;
+      tmp.reserve(p->n);
+      k_scatter1<<<(p->n + 255) / 256, 256, 0, c.stream>>>(p->dist.p, p->order.p, p->n, tmp.p);
+      IMB_CHECK(cudaMemcpyAsync(out, tmp.p, p->n * 8, cudaMemcpyDeviceToHost, c.stream));
+      IMB_CHECK(cudaStreamSynchronize(c.stream));
+      return;
+    }
     IMB_CHECK(cudaMemcpyAsync(out, p->dist.p, p->n * 8, cudaMemcpyDeviceToHost, c.stream));
     IMB_CHECK(cudaStreamSynchronize(c.stream));
   });
@@ -473,19 +519,38 @@ int im_volume_plan_set_level(im_volume_plan* p, int level, const double* ctrl, c
                              size_t nc, double D, int psi_kind, im_basis basis, int precision) {
   return guarded(p->ctx, [&](Context& c) {
     if (level < 0 || level >= 8) throw InvalidArgument("level index out of range (0..7)");
+    if (!p->reordered && precision != IM_EXACT && p->n) {
+      // one-time spatial layout of the resident mesh (grid cells of ~2R)
+      spatial_order(c, p->nodes.x.p, p->nodes.y.p, p->nodes.z.p, nullptr, p->n,
+                    basis.support_radius, p->order);
+      DBuf<double> tmp;
+      tmp.reserve(p->n);
+      const unsigned nb = (unsigned)((p->n + 255) / 256);
+      for (DBuf<double>* a : {&p->nodes.x, &p->nodes.y, &p->nodes.z, &p->dist}) {
+        k_gather<<<nb, 256, 0, c.stream>>>(a->p, p->order.p, p->n, tmp.p);
+        IMB_CHECK(cudaMemcpyAsync(a->p, tmp.p, p->n * 8, cudaMemcpyDeviceToDevice, c.stream));
+      }
+      IMB_CHECK(cudaStreamSynchronize(c.stream));
+      p->reordered = true;
+    }
     auto& L = p->levels[level];
     L.nc = nc;
     L.D = D;
     L.psi_kind = psi_kind;
-    L.tiles.reserve(6 * ctrl_padded(nc));
-    DBuf<double> stage;
-    stage.reserve(6 * std::max<size_t>(nc, 1));
-    if (nc) {
-      IMB_CHECK(cudaMemcpy(stage.p, ctrl, nc * 24, cudaMemcpyHostToDevice));
-      IMB_CHECK(cudaMemcpy(stage.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice));
+    if (precision == IM_EXACT) {
+      L.tiles.reserve(ctrl_tile_doubles(nc));
+      DBuf<double> stage;
+      stage.reserve(6 * std::max<size_t>(nc, 1));
+      if (nc) {
+        IMB_CHECK(cudaMemcpy(stage.p, ctrl, nc * 24, cudaMemcpyHostToDevice));
+        IMB_CHECK(cudaMemcpy(stage.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice));
+      }
+      pack_controls_aos(c, stage.p, stage.p + 3 * nc, nc, 1.0, L.tiles.p);
+      L.culled = false;
+    } else {
+      pack_controls_host(c, ctrl, alpha, nc, 1.0 / basis.support_radius, true, L.tiles, L.boxes);
+      L.culled = true;
     }
-    pack_controls_aos(c, stage.p, stage.p + 3 * nc, nc,
-                      precision == IM_EXACT ? 1.0 : 1.0 / basis.support_radius, L.tiles.p);
     IMB_CHECK(cudaStreamSynchronize(c.stream));
     p->n_levels = std::max(p->n_levels, level + 1);
   });
@@ -513,11 +578,18 @@ int im_volume_plan_run_steps(im_volume_plan* p, im_basis basis, int precision, i
       if (flush_l2) IMB_CHECK(cudaMemsetAsync(p->flush.p, s & 0xff, flush_bytes, c.stream));
       IMB_CHECK(cudaEventRecord(e0, c.stream));
       per_step = 0.0;
+      double last_D = NAN;
+      size_t last_na = 0;
       for (int l = 0; l < p->n_levels; ++l) {
         const auto& L = p->levels[l];
         if (L.D <= 0.0) continue;
-        const size_t na = compact_active(c, p->dist.p, p->n, L.D, p->active.p);
-        per_step += 3;
+        // compaction + spatial order, shared by consecutive levels with the same D
+        size_t na = last_na;
+        if (!(L.D == last_D)) {
+          na = compact_active(c, p->dist.p, p->n, L.D, p->active.p);
+          per_step += 3;
+          last_D = L.D, last_na = na;
+        }
         if (l < 4) stats[4 + l] = (double)na;
         VolumeArgs a;
         a.x = p->nodes.x.p, a.y = p->nodes.y.p, a.z = p->nodes.z.p;
@@ -527,6 +599,7 @@ int im_volume_plan_run_steps(im_volume_plan* p, im_basis basis, int precision, i
         a.D = L.D;
         a.psi_kind = L.psi_kind;
         a.tiles = L.tiles.p;
+        a.tile_box = L.culled ? L.boxes.p : nullptr;
         a.n_ctrl = L.nc;
         a.R = basis.support_radius;
         a.kind = basis.kind;

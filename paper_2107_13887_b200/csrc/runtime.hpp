@@ -130,12 +130,17 @@ void upload_points_indexed(Context& ctx, const double* host_xyz, const size_t* i
 // Padded to a multiple of kCtrlTile with inert controls.
 constexpr int kCtrlTile = 256;
 size_t ctrl_padded(size_t n);
+// doubles of device storage for the packed tiles of n controls
+size_t ctrl_tile_doubles(size_t n);
 void pack_controls(Context& ctx, const double* d_cx, const double* d_cy, const double* d_cz,
                    const double* d_ax, const double* d_ay, const double* d_az, size_t n,
                    double scale, double* d_tiles);
 
 void pack_controls_aos(Context& ctx, const double* d_ctrl_aos, const double* d_alpha_aos, size_t n,
                        double scale, double* d_tiles);
+// Host packing for the fast path (Morton-sorted tiles + per-tile boxes).
+void pack_controls_host(Context& ctx, const double* host_ctrl, const double* host_alpha, size_t n,
+                        double scale, bool sort, DBuf<double>& tiles, DBuf<double>& boxes);
 
 enum class Precision : int { Exact = 0, Fast64 = 1, Fast32 = 2 };
 
@@ -143,6 +148,7 @@ struct VolumeArgs {
   // points (SoA); optional gather list of active node ids (nullptr = identity)
   const double *x = nullptr, *y = nullptr, *z = nullptr;
   const uint32_t* active = nullptr;
+  const uint32_t* perm = nullptr;  // spatial processing order of the active positions (fast path)
   size_t n_active = 0;
   // wall distances per node (nullptr = psi == 1, i.e. D = inf)
   const double* dist = nullptr;
@@ -150,6 +156,7 @@ struct VolumeArgs {
   int psi_kind = 0;
   // controls
   const double* tiles = nullptr;  // packed (pack_controls)
+  const double* tile_box = nullptr;  // per-tile boxes (fast path culling) or null
   size_t n_ctrl = 0;
   double R = 1.0;
   int kind = 1;
@@ -167,6 +174,11 @@ void launch_volume(Context& ctx, const VolumeArgs& a);
 // Stable compaction of {i : dist[i] < D} (wall_distance.cpp:56-58).  Writes
 // ascending node ids to d_out and returns the count (synchronises).
 size_t compact_active(Context& ctx, const double* d_dist, size_t n, double D, uint32_t* d_out);
+
+// Device permutation of the n active positions ordered by grid cells of
+// edge ~2R (spatially compact CTAs for the tile culling).
+void spatial_order(Context& ctx, const double* x, const double* y, const double* z,
+                   const uint32_t* active, size_t n, double R, DBuf<uint32_t>& perm);
 
 // Number of (active node, control) pairs with |r_v - r_c| < R (fast path
 // arithmetic, tiles packed with scale 1/R).
