@@ -408,51 +408,65 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     *n_entries = 0;
     const double D = wf->support_distance;
     if (D <= 0.0 || n_nodes == 0) return;  // wall_distance.cpp:54
-    DPoints dn;
-    upload_points(c, nodes, n_nodes, dn);
-    DBuf<double> dd, staging, tiles, vals;
-    DBuf<uint32_t> active;
-    dd.reserve(n_nodes);
-    active.reserve(n_nodes);
-    IMB_CHECK(cudaMemcpyAsync(dd.p, dist, n_nodes * 8, cudaMemcpyHostToDevice, c.stream));
-    staging.reserve(6 * std::max<size_t>(nc, 1));
-    tiles.reserve(ctrl_tile_doubles(nc));
-    if (nc) {
-      IMB_CHECK(cudaMemcpyAsync(staging.p, ctrl, nc * 24, cudaMemcpyHostToDevice, c.stream));
-      IMB_CHECK(cudaMemcpyAsync(staging.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice, c.stream));
-    }
+    // device buffers come from the context's grow-only slots: no cudaMalloc /
+    // cudaFree on this path
+    double* dx = c.buf<double>(Context::kSlotNodesX, n_nodes);
+    double* dy = c.buf<double>(Context::kSlotNodesY, n_nodes);
+    double* dz = c.buf<double>(Context::kSlotNodesZ, n_nodes);
+    double* dd = c.buf<double>(Context::kSlotDist, n_nodes);
+    uint32_t* active = c.buf<uint32_t>(Context::kSlotActive, n_nodes);
+    double* stage = c.buf<double>(Context::kSlotStage, 3 * n_nodes + 6 * nc);
+    IMB_CHECK(cudaMemcpyAsync(stage, nodes, n_nodes * 24, cudaMemcpyHostToDevice, c.stream));
+    aos_to_soa(c, stage, n_nodes, dx, dy, dz);
+    IMB_CHECK(cudaMemcpyAsync(dd, dist, n_nodes * 8, cudaMemcpyHostToDevice, c.stream));
     const bool exact = precision == IM_EXACT;
-    DBuf<double> boxes;
-    if (!exact)
+    double* tiles = c.buf<double>(Context::kSlotTiles, ctrl_tile_doubles(nc));
+    double* boxes = nullptr;
+    if (exact) {
+      double* cs = stage + 3 * n_nodes;
+      if (nc) {
+        IMB_CHECK(cudaMemcpyAsync(cs, ctrl, nc * 24, cudaMemcpyHostToDevice, c.stream));
+        IMB_CHECK(cudaMemcpyAsync(cs + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice, c.stream));
+      }
+      pack_controls_aos(c, cs, cs + 3 * nc, nc, 1.0, tiles);
+    } else {
+      boxes = c.buf<double>(Context::kSlotBoxes, 6 * (ctrl_padded(nc) / kCtrlTile));
       pack_controls_host(c, ctrl, alpha, nc, 1.0 / basis.support_radius, true, tiles, boxes);
+    }
+    // planar input (z == 0 everywhere) runs the 2-D kernel
+    bool planar = true;
+    for (size_t i = 0; i < n_nodes && planar; ++i) planar = nodes[3 * i + 2] == 0.0;
+    for (size_t i = 0; i < nc && planar; ++i) planar = ctrl[3 * i + 2] == 0.0 && alpha[3 * i + 2] == 0.0;
     EventTimer tm(c.stream);
-    if (exact) pack_controls_aos(c, staging.p, staging.p + 3 * nc, nc, 1.0, tiles.p);
-    const size_t na = compact_active(c, dd.p, n_nodes, D, active.p);
-    DBuf<uint32_t> perm;
-    if (!exact) spatial_order(c, dn.x.p, dn.y.p, dn.z.p, active.p, na, basis.support_radius, perm);
-    vals.reserve(3 * std::max<size_t>(na, 1));
+    const size_t na = compact_active(c, dd, n_nodes, D, active);
+    uint32_t* perm = nullptr;
+    if (!exact && na) {
+      perm = c.buf<uint32_t>(Context::kSlotPerm, na);
+      spatial_order(c, dx, dy, dz, active, na, basis.support_radius, perm);
+    }
+    double* vals = c.buf<double>(Context::kSlotVals, 3 * std::max<size_t>(na, 1));
     VolumeArgs a;
-    a.x = dn.x.p, a.y = dn.y.p, a.z = dn.z.p;
-    a.active = active.p;
+    a.x = dx, a.y = dy, a.z = dz;
+    a.active = active;
     a.n_active = na;
-    a.dist = dd.p;
+    a.dist = dd;
     a.D = D;
     a.psi_kind = wf->psi_kind;
-    a.tiles = tiles.p;
+    a.tiles = tiles;
     a.n_ctrl = nc;
     a.R = basis.support_radius;
     a.kind = basis.kind;
-    a.dim = 3;
+    a.dim = planar && !exact ? 2 : 3;
     a.precision = exact ? Precision::Exact : Precision::Fast64;
-    a.out_val = vals.p;
-    a.tile_box = exact ? nullptr : boxes.p;
-    a.perm = exact ? nullptr : perm.p;
+    a.out_val = vals;
+    a.tile_box = boxes;
+    a.perm = perm;
     launch_volume(c, a);
     c.last_kernel_ms = tm.stop();
-    std::vector<uint32_t> idx(na);
+    uint32_t* idx = reinterpret_cast<uint32_t*>(c.pinned.reserve(na * 4 + 16));
     if (na) {
-      IMB_CHECK(cudaMemcpyAsync(idx.data(), active.p, na * 4, cudaMemcpyDeviceToHost, c.stream));
-      IMB_CHECK(cudaMemcpyAsync(entry_values, vals.p, na * 24, cudaMemcpyDeviceToHost, c.stream));
+      IMB_CHECK(cudaMemcpyAsync(idx, active, na * 4, cudaMemcpyDeviceToHost, c.stream));
+      IMB_CHECK(cudaMemcpyAsync(entry_values, vals, na * 24, cudaMemcpyDeviceToHost, c.stream));
       IMB_CHECK(cudaStreamSynchronize(c.stream));
     }
     for (size_t i = 0; i < na; ++i) entry_nodes[i] = idx[i];

@@ -113,6 +113,18 @@ struct Context {
   DBuf<unsigned char> scratch;
   HBuf<unsigned char> pinned;
   double last_kernel_ms = 0.0;
+  // Grow-only device scratch slots reused across calls (no cudaMalloc /
+  // cudaFree -- which synchronises the device -- on the hot path).
+  enum Slot : int {
+    kSlotNodesX, kSlotNodesY, kSlotNodesZ, kSlotDist, kSlotActive, kSlotPerm, kSlotVals,
+    kSlotTiles, kSlotBoxes, kSlotStage, kSlotCell, kSlotCounts, kSlotStart, kSlotBox,
+    kSlotScanA, kSlotScanB, kSlotCount
+  };
+  DBuf<unsigned char> slots[kSlotCount];
+  template <class T>
+  T* buf(Slot s, size_t count) {
+    return reinterpret_cast<T*>(slots[s].reserve(count * sizeof(T) + 16));
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -141,6 +153,10 @@ void pack_controls_aos(Context& ctx, const double* d_ctrl_aos, const double* d_a
 // Host packing for the fast path (Morton-sorted tiles + per-tile boxes).
 void pack_controls_host(Context& ctx, const double* host_ctrl, const double* host_alpha, size_t n,
                         double scale, bool sort, DBuf<double>& tiles, DBuf<double>& boxes);
+void pack_controls_host(Context& ctx, const double* host_ctrl, const double* host_alpha, size_t n,
+                        double scale, bool sort, double* d_tiles, double* d_boxes);
+// device AoS -> SoA
+void aos_to_soa(Context& ctx, const double* d_aos, size_t n, double* x, double* y, double* z);
 
 enum class Precision : int { Exact = 0, Fast64 = 1, Fast32 = 2 };
 
@@ -179,6 +195,10 @@ size_t compact_active(Context& ctx, const double* d_dist, size_t n, double D, ui
 // edge ~2R (spatially compact CTAs for the tile culling).
 void spatial_order(Context& ctx, const double* x, const double* y, const double* z,
                    const uint32_t* active, size_t n, double R, DBuf<uint32_t>& perm);
+// Asynchronous variant (no host synchronisation, context scratch).
+void spatial_order(Context& ctx, const double* x, const double* y, const double* z,
+                   const uint32_t* active, size_t n, double R, uint32_t* perm);
+void scan_u32_to_u64_async(Context& ctx, const unsigned int* in, size_t n, unsigned long long* out);
 
 // Number of (active node, control) pairs with |r_v - r_c| < R (fast path
 // arithmetic, tiles packed with scale 1/R).
