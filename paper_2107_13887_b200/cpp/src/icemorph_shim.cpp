@@ -1,0 +1,298 @@
+// icemorph_shim.cpp — the reference's public C++ API (icemorph/icemorph.hpp)
+// over the B200 C-ABI (include/icemorph_b200.h).  Host-side glue only:
+// argument marshalling, the reference's exceptions, and the scalar helpers
+// (eval_wendland / eval_basis / wall functions) that the reference also
+// evaluates on the host.  Every hot-path call goes to the device.
+#include <iomanip>
+#include <ostream>
+#include <unordered_set>
+
+#include "../../../include/icemorph_b200.h"
+#include "icemorph/icemorph.hpp"
+
+namespace icemorph {
+namespace {
+
+// One context per host thread: calls from different threads never share a
+// stream or scratch (the reference's reentrancy).
+im_context* ctx() {
+  thread_local struct Holder {
+    im_context* c = nullptr;
+    Holder() { im_context_create(&c, 0); }
+    ~Holder() { im_context_destroy(c); }
+  } h;
+  return h.c;
+}
+
+void check(int rc) {
+  if (rc == IM_OK) return;
+  const std::string msg = im_last_error(ctx());
+  if (rc == IM_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (rc == IM_SOLVE_ERROR) throw SolveError(msg);
+  throw std::runtime_error(msg);
+}
+
+im_basis to_c(const BasisFunction& b) { return {static_cast<int>(b.kind), b.support_radius}; }
+
+im_greedy_config to_c(const GreedyConfig& g) {
+  return {g.tolerance, g.max_levels, g.max_points_per_level, to_c(g.basis)};
+}
+
+const double* xyz(std::span<const Vec3> v) { return v.empty() ? nullptr : &v[0].x; }
+
+}  // namespace
+
+// rbf.cpp:10-26
+WendlandKind wendland_kind_from_string(const std::string& name) {
+  if (name == "c0" || name == "C0") return WendlandKind::C0;
+  if (name == "c2" || name == "C2") return WendlandKind::C2;
+  if (name == "c4" || name == "C4") return WendlandKind::C4;
+  if (name == "c6" || name == "C6") return WendlandKind::C6;
+  throw std::invalid_argument("unknown basis function '" + name + "' (expected c0, c2, c4 or c6)");
+}
+
+std::string_view wendland_kind_name(WendlandKind kind) {
+  static const char* names[] = {"c0", "c2", "c4", "c6"};
+  const int k = static_cast<int>(kind);
+  return k >= 0 && k < 4 ? names[k] : "?";
+}
+
+double eval_wendland(WendlandKind kind, double eta) {
+  return im_eval_wendland(static_cast<int>(kind), eta);
+}
+
+double eval_basis(const BasisFunction& basis, double d) { return im_eval_basis(to_c(basis), d); }
+
+WeightSet solve_weights(std::span<const Vec3> points, std::span<const Vec3> displacements,
+                        const BasisFunction& basis) {
+  if (points.size() != displacements.size())
+    throw std::invalid_argument("point and displacement counts differ");
+  WeightSet w;
+  w.control_positions.assign(points.begin(), points.end());
+  w.alpha.assign(points.size(), Vec3{});
+  check(im_solve_weights(ctx(), xyz(points), xyz(displacements), points.size(), to_c(basis),
+                         w.alpha.empty() ? nullptr : &w.alpha[0].x));
+  return w;
+}
+
+std::vector<Vec3> eval_interpolant(const WeightSet& w, const BasisFunction& basis,
+                                   std::span<const Vec3> queries) {
+  std::vector<Vec3> out(queries.size());
+  check(im_eval_interpolant(ctx(), xyz(w.control_positions), xyz(w.alpha), w.size(), to_c(basis),
+                            xyz(queries), queries.size(), IM_EXACT,
+                            out.empty() ? nullptr : &out[0].x));
+  return out;
+}
+
+Vec3 eval_interpolant(const WeightSet& w, const BasisFunction& basis, const Vec3& query) {
+  return eval_interpolant(w, basis, std::span<const Vec3>(&query, 1))[0];
+}
+
+LevelResult greedy_level(std::span<const Vec3> pos, std::span<const Vec3> target,
+                         const GreedyConfig& config, std::size_t level_index) {
+  if (target.size() != pos.size())
+    throw std::invalid_argument("target size does not match surface size");
+  const std::size_t m = std::max<std::size_t>(1, std::min(config.max_points_per_level, pos.size()));
+  const im_greedy_config cfg = to_c(config);
+  std::vector<std::size_t> idx(m), rp(m);
+  std::vector<Vec3> alpha(m);
+  std::vector<double> re(m), rs(m);
+  LevelResult r;
+  r.residual.resize(pos.size());
+  size_t nc = 0, nrec = 0;
+  double achieved = 0, tmax = 0, el = 0;
+  int cap_hit = 0;
+  check(im_greedy_level(ctx(), xyz(pos), xyz(target), pos.size(), &cfg, level_index, idx.data(),
+                        &alpha[0].x, &nc, &achieved, &cap_hit, &tmax, &el, rp.data(), re.data(),
+                        rs.data(), &nrec, r.residual.empty() ? nullptr : &r.residual[0].x));
+  r.level.level = level_index;
+  r.level.control_indices.assign(idx.begin(), idx.begin() + nc);
+  for (std::size_t c : r.level.control_indices) r.level.weights.control_positions.push_back(pos[c]);
+  r.level.weights.alpha.assign(alpha.begin(), alpha.begin() + nc);
+  r.level.achieved_error = achieved;
+  r.level.cap_hit = cap_hit != 0;
+  r.level.target_max = tmax;
+  r.level.elapsed_seconds = el;
+  for (std::size_t s = 0; s < nrec; ++s) r.record.samples.push_back({rp[s], re[s], rs[s]});
+  return r;
+}
+
+MultilevelResult run_multilevel(std::span<const Vec3> pos, std::span<const Vec3> target,
+                                const GreedyConfig& config) {
+  if (target.size() != pos.size())
+    throw std::invalid_argument("target size does not match surface size");
+  const std::size_t m = std::max<std::size_t>(1, std::min(config.max_points_per_level, pos.size()));
+  const std::size_t L = std::max<std::size_t>(1, config.max_levels);
+  const im_greedy_config cfg = to_c(config);
+  std::vector<std::size_t> nc(L), idx(L * m), nrec(L);
+  std::vector<Vec3> alpha(L * m);
+  std::vector<double> ach(L), ltm(L), el(L), rerr(L * m);
+  std::vector<int> caph(L);
+  size_t nl = 0;
+  MultilevelResult r;
+  r.final_residual.resize(pos.size());
+  check(im_run_multilevel(ctx(), xyz(pos), xyz(target), pos.size(), &cfg, &nl, nc.data(),
+                          idx.data(), &alpha[0].x, ach.data(), caph.data(), ltm.data(), el.data(),
+                          nrec.data(), rerr.data(), &r.target_max,
+                          r.final_residual.empty() ? nullptr : &r.final_residual[0].x));
+  for (std::size_t l = 0; l < nl; ++l) {
+    RbfLevel lv;
+    lv.level = l;
+    lv.control_indices.assign(idx.begin() + l * m, idx.begin() + l * m + nc[l]);
+    for (std::size_t c : lv.control_indices) lv.weights.control_positions.push_back(pos[c]);
+    lv.weights.alpha.assign(alpha.begin() + l * m, alpha.begin() + l * m + nc[l]);
+    lv.achieved_error = ach[l];
+    lv.cap_hit = caph[l] != 0;
+    lv.target_max = ltm[l];
+    lv.elapsed_seconds = el[l];
+    ConvergenceRecord rec;
+    for (std::size_t s = 0; s < nrec[l]; ++s) rec.samples.push_back({s + 1, rerr[l * m + s], 0.0});
+    r.levels.push_back(std::move(lv));
+    r.records.push_back(std::move(rec));
+  }
+  return r;
+}
+
+void write_convergence_csv_header(std::ostream& out) { out << "level,points,error,seconds\n"; }
+
+void append_convergence_csv(std::ostream& out, std::size_t level, const ConvergenceRecord& rec) {
+  for (const auto& s : rec.samples)
+    out << level << ',' << s.points << ',' << std::setprecision(17) << s.error << ','
+        << std::setprecision(6) << s.seconds << "\n";
+}
+
+const Marker* Mesh::find_marker(std::string_view name) const {
+  for (const auto& m : markers)
+    if (m.name == name) return &m;
+  return nullptr;
+}
+
+const Marker& Mesh::marker(std::string_view name) const {
+  const Marker* m = find_marker(name);
+  if (!m) throw std::invalid_argument("mesh has no marker named '" + std::string(name) + "'");
+  return *m;
+}
+
+double DisplacementField::max_magnitude() const {
+  double m = 0.0;
+  for (const auto& [n, d] : entries) m = std::max(m, d.norm());
+  return m;
+}
+
+DistanceIndex build_distance_index(const Mesh& mesh, const std::string& marker) {
+  return build_distance_index(mesh, mesh.marker(marker).nodes);
+}
+
+DistanceIndex build_distance_index(const Mesh& mesh, const std::vector<std::size_t>& surface) {
+  DistanceIndex idx;
+  idx.distances.resize(mesh.nodes.size());
+  check(im_build_distance_index(ctx(), xyz(mesh.nodes), mesh.nodes.size(), mesh.dim,
+                                surface.data(), surface.size(), idx.distances.data()));
+  return idx;
+}
+
+WallFunction make_wall_function(double k, double level_target_max) {
+  im_wall_function wf{};
+  if (im_make_wall_function(k, level_target_max, &wf) != IM_OK)
+    throw std::invalid_argument("volume reduction factor must be positive");
+  return {wf.reduction_factor, wf.support_distance, wf.psi_kind};
+}
+
+double eval_wall_function(const WallFunction& wf, double d) {
+  const im_wall_function w{wf.reduction_factor, wf.support_distance, wf.psi_kind};
+  return im_eval_wall_function(&w, d);
+}
+
+VolumeUpdate update_volume(const Mesh& mesh, const RbfLevel& level, const DistanceIndex& index,
+                           const WallFunction& wf, const BasisFunction& basis) {
+  if (index.distances.size() != mesh.nodes.size())
+    throw std::invalid_argument("distance index does not match the mesh");
+  const std::size_t n = mesh.nodes.size();
+  std::vector<std::size_t> nodes(n);
+  std::vector<Vec3> values(n);
+  size_t k = 0;
+  const im_wall_function w{wf.reduction_factor, wf.support_distance, wf.psi_kind};
+  check(im_update_volume(ctx(), xyz(mesh.nodes), n, index.distances.data(),
+                         xyz(level.weights.control_positions), xyz(level.weights.alpha),
+                         level.weights.size(), &w, to_c(basis), IM_EXACT, nodes.data(),
+                         values.empty() ? nullptr : &values[0].x, &k));
+  VolumeUpdate u;
+  u.entries.reserve(k);
+  for (std::size_t i = 0; i < k; ++i) u.entries.emplace_back(nodes[i], values[i]);
+  return u;
+}
+
+std::size_t DeformationReport::total_control_points() const {
+  std::size_t t = 0;
+  for (const auto& l : levels) t += l.points;
+  return t;
+}
+
+std::pair<Mesh, DeformationReport> deform(const Mesh& mesh, const DisplacementField& disp,
+                                          const DeformationConfig& config) {
+  const Marker& marker = mesh.marker(disp.patch);
+  if (marker.nodes.empty())
+    throw std::invalid_argument("marker '" + disp.patch + "' has no nodes");
+  std::vector<std::size_t> pinned;
+  for (const auto& name : config.fixed_markers)
+    for (std::size_t n : mesh.marker(name).nodes) pinned.push_back(n);
+  std::vector<Vec3> d(marker.nodes.size());
+  for (std::size_t i = 0; i < marker.nodes.size(); ++i) d[i] = disp.at(marker.nodes[i]);
+  const im_deform_config cfg{to_c(config.greedy), config.volume_k, config.support_distance,
+                             config.psi_kind, config.precision};
+  Mesh out = mesh;
+  im_deform_report rep{};
+  const std::size_t L = std::max<std::size_t>(1, config.greedy.max_levels);
+  std::vector<std::size_t> pts(L), touched(L);
+  std::vector<double> ach(L), sup(L), sec(L);
+  std::vector<int> caph(L);
+  check(im_deform(ctx(), xyz(mesh.nodes), mesh.nodes.size(), mesh.dim, marker.nodes.data(),
+                  marker.nodes.size(), &d[0].x, pinned.empty() ? nullptr : pinned.data(),
+                  pinned.size(), &cfg, out.nodes.empty() ? nullptr : &out.nodes[0].x, &rep,
+                  pts.data(), ach.data(), caph.data(), sup.data(), touched.data(), sec.data()));
+  DeformationReport r;
+  r.marker = disp.patch;
+  for (std::size_t l = 0; l < rep.n_levels; ++l) {
+    LevelSummary s;
+    s.level = l;
+    s.points = pts[l];
+    s.achieved_error = ach[l];
+    s.cap_hit = caph[l] != 0;
+    s.support_distance = sup[l];
+    s.touched_nodes = touched[l];
+    s.seconds = sec[l];
+    r.levels.push_back(std::move(s));
+  }
+  r.target_max = rep.target_max;
+  r.surface_max_error = rep.surface_max_error;
+  r.surface_mean_error = rep.surface_mean_error;
+  r.total_seconds = rep.total_seconds;
+  return {std::move(out), std::move(r)};
+}
+
+void write_summary(const DeformationReport& report, std::ostream& out) {
+  out << std::setprecision(17);
+  out << "marker: " << report.marker << "\n";
+  out << "levels: " << report.levels.size() << "\n";
+  out << "total_control_points: " << report.total_control_points() << "\n";
+  out << "target_max: " << report.target_max << "\n";
+  out << "surface_max_error: " << report.surface_max_error << "\n";
+  out << "surface_mean_error: " << report.surface_mean_error << "\n";
+  out << "inverted_elements: " << report.inverted_elements << "\n";
+  out << "total_seconds: " << std::setprecision(6) << report.total_seconds << std::setprecision(17)
+      << "\n";
+  for (const auto& l : report.levels) {
+    const std::string p = "level_" + std::to_string(l.level) + "_";
+    out << p << "points: " << l.points << "\n" << p << "error: " << l.achieved_error << "\n"
+        << p << "cap_hit: " << (l.cap_hit ? 1 : 0) << "\n" << p << "support_distance: "
+        << l.support_distance << "\n" << p << "touched_nodes: " << l.touched_nodes << "\n" << p
+        << "seconds: " << std::setprecision(6) << l.seconds << std::setprecision(17) << "\n";
+  }
+}
+
+void write_convergence_csv(const DeformationReport& report, std::ostream& out) {
+  write_convergence_csv_header(out);
+  for (const auto& l : report.levels) append_convergence_csv(out, l.level, l.record);
+}
+
+}  // namespace icemorph

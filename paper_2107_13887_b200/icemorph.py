@@ -1,0 +1,178 @@
+"""Python mirror of the reference's ``icemorph`` module for the hot path
+(proj/python/bindings.cpp:34-242, re-exported by proj/python/icemorph/__init__.py),
+backed by the B200 C-ABI through :mod:`paper_2107_13887_b200.capi`.
+
+Same names, argument meaning and error behaviour as the reference binding:
+``eval_basis``, ``solve_weights``, ``eval_interpolant``, ``deform`` with
+``Mesh`` / ``DisplacementField`` / ``DeformationConfig`` / ``DeformationReport``
+/ ``LevelSummary``; ``ValueError`` for std::invalid_argument and
+``RuntimeError`` (``capi.SolveError``) for icemorph::SolveError, as pybind11
+maps them.  Mesh I/O, generators and quality metrics are out of scope; a
+``Mesh`` is built from arrays (``Mesh(dim, nodes, markers)``) instead of
+``read_su2`` / ``gen_airfoil_mesh``.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import capi
+
+_ctx = None
+
+
+def _context() -> capi.Context:
+    global _ctx
+    if _ctx is None:
+        _ctx = capi.Context(0)
+    return _ctx
+
+
+def _kind(name: str) -> str:
+    if name not in ("c0", "c2", "c4", "c6", "C0", "C2", "C4", "C6"):
+        raise ValueError(f"unknown basis function '{name}' (expected c0, c2, c4 or c6)")
+    return name.lower()
+
+
+def eval_basis(kind: str, support_radius: float, distance: float) -> float:
+    """bindings.cpp:199-204 -> eval_basis (rbf.cpp:52-54)."""
+    lib = capi.load_library()
+    return lib.im_eval_basis(capi.basis(_kind(kind), support_radius), float(distance))
+
+
+def solve_weights(points, displacements, kind="c2", support_radius=1.0):
+    """bindings.cpp:205-219 -> solve_weights (rbf.cpp:144-193); list of [x,y,z]."""
+    return _context().solve_weights(points, displacements, _kind(kind), support_radius).tolist()
+
+
+def eval_interpolant(points, alpha, kind, support_radius, query):
+    """bindings.cpp:220-232 -> eval_interpolant (rbf.cpp:195-203) for one query."""
+    out = _context().eval_interpolant(points, alpha, _kind(kind), support_radius, [query],
+                                      capi.EXACT)
+    return list(out[0])
+
+
+class Mesh:
+    """Node array + named markers (the part of the reference Mesh the hot path
+    reads, mesh.hpp:42-58)."""
+
+    def __init__(self, dim: int, nodes, markers: dict):
+        self.dim = int(dim)
+        self._nodes = capi.xyz(nodes)
+        self._markers = {k: [int(i) for i in v] for k, v in markers.items()}
+
+    @property
+    def num_nodes(self) -> int:
+        return len(self._nodes)
+
+    def node(self, i):
+        if not 0 <= i < len(self._nodes):
+            raise IndexError(i)
+        return list(self._nodes[i])
+
+    def nodes(self):
+        return [list(p) for p in self._nodes]
+
+    def marker_names(self):
+        return list(self._markers)
+
+    def marker_nodes(self, name: str):
+        if name not in self._markers:
+            raise ValueError(f"mesh has no marker named '{name}'")
+        return list(self._markers[name])
+
+
+class DisplacementField:
+    """bindings.cpp:66-85 (mesh_io.hpp:25-34)."""
+
+    def __init__(self, patch: str):
+        self.patch = patch
+        self._entries: dict[int, tuple] = {}
+
+    def set(self, node: int, dx: float, dy: float, dz: float = 0.0):
+        self._entries[int(node)] = (float(dx), float(dy), float(dz))
+
+    def entries(self):
+        return dict(self._entries)
+
+    def at(self, node: int):
+        return self._entries.get(int(node), (0.0, 0.0, 0.0))
+
+    def max_magnitude(self) -> float:
+        return max((math.sqrt(x * x + y * y + z * z) for x, y, z in self._entries.values()),
+                   default=0.0)
+
+
+class DeformationConfig:
+    """bindings.cpp:87-117 properties (pipeline.hpp:18-23) plus the additive
+    fields: support_distance (None = reference D_l = volume_k * target_max_l),
+    psi ('linear' | 'c2'), precision ('exact' | 'fp64')."""
+
+    def __init__(self):
+        self.basis = "c2"
+        self.support_radius = 1.0
+        self.tolerance = 0.1
+        self.levels = 5
+        self.max_points_per_level = 5000
+        self.volume_k = 5.0
+        self.fixed_markers: list[str] = []
+        self.compute_quality = True  # accepted; quality metrics are out of scope
+        self.support_distance = None
+        self.psi = "linear"
+        self.precision = "exact"
+
+
+@dataclass
+class LevelSummary:
+    level: int
+    points: int
+    achieved_error: float
+    cap_hit: bool
+    support_distance: float
+    touched_nodes: int
+    seconds: float
+
+
+@dataclass
+class DeformationReport:
+    marker: str
+    levels: list = field(default_factory=list)
+    target_max: float = 0.0
+    surface_max_error: float = 0.0
+    surface_mean_error: float = 0.0
+    inverted_elements: int = 0
+    quality_before: object = None
+    quality_after: object = None
+    total_seconds: float = 0.0
+
+    @property
+    def total_control_points(self) -> int:
+        return sum(l.points for l in self.levels)
+
+
+def deform(mesh: Mesh, displacement: DisplacementField, config: DeformationConfig):
+    """bindings.cpp:191-193 -> deform (pipeline.cpp:19-106).  Returns
+    (deformed_mesh, report); the input mesh is left unchanged."""
+    patch = mesh.marker_nodes(displacement.patch)
+    if not patch:
+        raise ValueError(f"marker '{displacement.patch}' has no nodes")
+    pinned = [n for name in config.fixed_markers for n in mesh.marker_nodes(name)]
+    disp = np.array([displacement.at(n) for n in patch], dtype=np.float64).reshape(-1, 3)
+    D = -1.0 if config.support_distance is None else float(config.support_distance)
+    r = _context().deform(mesh._nodes, mesh.dim, patch, disp, pinned, config.tolerance,
+                          config.levels, config.max_points_per_level, _kind(config.basis),
+                          config.support_radius, config.volume_k, D,
+                          1 if config.psi in ("c2", "wendland_c2") else 0,
+                          capi.EXACT if config.precision == "exact" else capi.FP64)
+    out = Mesh(mesh.dim, r["nodes"], mesh._markers)
+    rep = DeformationReport(marker=displacement.patch, target_max=r["target_max"],
+                            surface_max_error=r["surface_max_error"],
+                            surface_mean_error=r["surface_mean_error"],
+                            total_seconds=r["total_seconds"])
+    for l in range(len(r["points"])):
+        rep.levels.append(LevelSummary(l, int(r["points"][l]), float(r["achieved"][l]),
+                                       bool(r["cap_hit"][l]), float(r["support"][l]),
+                                       int(r["touched"][l]), float(r["seconds"][l])))
+    return out, rep

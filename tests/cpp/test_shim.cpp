@@ -1,0 +1,108 @@
+// C++ client of the reference API (icemorph/icemorph.hpp) backed by the B200
+// library: the reference tests' known-answer values, checked through the C++
+// shim exactly as a reference caller would use it.  Exit code 0 = all passed.
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "icemorph/icemorph.hpp"
+
+using namespace icemorph;
+
+static int failures = 0;
+#define CHECK(cond)                                                   \
+  do {                                                                \
+    if (!(cond)) {                                                    \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);     \
+      ++failures;                                                     \
+    }                                                                 \
+  } while (0)
+
+int main() {
+  // rbf KATs (test_rbf.cpp:40-52, 74-80)
+  CHECK(eval_wendland(WendlandKind::C2, 0.5) == 0.1875);
+  CHECK(eval_wendland(WendlandKind::C0, 0.5) == 0.25);
+  CHECK(eval_basis({WendlandKind::C2, 2.0}, 1.0) == 0.1875);
+  // two-point solve (test_rbf.cpp:96-119)
+  const BasisFunction b2{WendlandKind::C2, 2.0};
+  const std::vector<Vec3> two{{0.0, 0.0}, {1.0, 0.0}};
+  const WeightSet w = solve_weights(two, std::vector<Vec3>{{1.0, 0.0}, {0.0, 0.0}}, b2);
+  const double bb = 0.1875;
+  CHECK(std::abs(w.alpha[0].x - 1.0 / (1.0 - bb * bb)) < 1e-12);
+  CHECK(std::abs(w.alpha[1].x + bb / (1.0 - bb * bb)) < 1e-12);
+  CHECK(std::abs(eval_interpolant(w, b2, Vec3{0.5, 0.0}).x - 0.6328125 / 1.1875) < 1e-12);
+  // duplicate points -> SolveError naming the pair (test_rbf.cpp:223-229)
+  bool threw = false;
+  try {
+    solve_weights(std::vector<Vec3>{{0, 0}, {1e-18, 0}}, std::vector<Vec3>{{1, 0}, {2, 0}},
+                  {WendlandKind::C2, 1.0});
+  } catch (const SolveError& e) {
+    threw = std::string(e.what()).find("points 0 and 1") != std::string::npos;
+  }
+  CHECK(threw);
+  // greedy: three collinear points (test_greedy.cpp:38-51)
+  GreedyConfig gc;
+  gc.tolerance = 0.1;
+  gc.max_levels = 1;
+  gc.basis = b2;
+  const auto g = greedy_level(std::vector<Vec3>{{0, 0}, {0.5, 0}, {1, 0}},
+                              std::vector<Vec3>{{0, 0}, {0, 1}, {0, 0}}, gc);
+  CHECK(g.level.control_indices.size() >= 2 && g.level.control_indices[0] == 0 &&
+        g.level.control_indices[1] == 1);
+  CHECK(g.level.achieved_error < 0.1);
+  CHECK(g.record.samples.size() == g.level.control_indices.size());
+  // wall distance (test_wall_distance.cpp:29-39)
+  Mesh mesh;
+  mesh.dim = 2;
+  mesh.nodes = {{0.0, 0.0}, {1.0, 0.0}, {0.5, 1.0}, {4.0, 0.0}};
+  const DistanceIndex idx = build_distance_index(mesh, std::vector<std::size_t>{0, 1});
+  CHECK(idx.distances[0] == 0.0 && idx.distances[1] == 0.0);
+  CHECK(std::abs(idx.distances[2] - std::sqrt(1.25)) < 1e-15);
+  CHECK(idx.distances[3] == 3.0);
+  // wall taper (test_wall_distance.cpp:49-60)
+  const WallFunction wf = make_wall_function(5.0, 0.02);
+  CHECK(std::abs(eval_wall_function(wf, 0.05) - 0.5) < 1e-12);
+  CHECK(eval_wall_function(wf, 0.1) == 0.0);
+  // update_volume (test_wall_distance.cpp:62-90)
+  Mesh m2;
+  m2.dim = 2;
+  m2.nodes = {{0.0, 0.0}, {0.0, 0.05}, {0.0, 0.2}, {0.0, 5.0}};
+  const DistanceIndex i2 = build_distance_index(m2, std::vector<std::size_t>{0});
+  RbfLevel lvl;
+  lvl.weights.control_positions = {{0.0, 0.0}};
+  lvl.weights.alpha = {{0.0, 0.7, 0.0}};
+  lvl.target_max = 0.02;
+  const VolumeUpdate u = update_volume(m2, lvl, i2, make_wall_function(5.0, 0.02), b2);
+  CHECK(u.entries.size() == 2);
+  CHECK(u.entries[0].first == 0 && u.entries[0].second == lvl.weights.alpha[0]);
+  CHECK(u.entries[1].first == 1 &&
+        std::abs(u.entries[1].second.y - 0.5 * 0.7 * eval_basis(b2, 0.05)) < 1e-14);
+  // deform on a small ring mesh with a pinned outer ring (test_pipeline.cpp:61-77)
+  Mesh ring;
+  ring.dim = 2;
+  const int n = 64;
+  Marker inner{"wall", {}, {}}, outer{"far", {}, {}};
+  for (int layer = 0; layer < 6; ++layer)
+    for (int j = 0; j < n; ++j) {
+      const double t = 2 * M_PI * j / n, r = 1.0 + 0.5 * layer;
+      ring.nodes.push_back({r * std::cos(t), r * std::sin(t)});
+      if (layer == 0) inner.nodes.push_back(ring.nodes.size() - 1);
+      if (layer == 5) outer.nodes.push_back(ring.nodes.size() - 1);
+    }
+  ring.markers = {inner, outer};
+  DisplacementField f;
+  f.patch = "wall";
+  for (std::size_t k : inner.nodes)
+    f.entries[k] = Vec3{0.0, 0.02 * std::sin(3.0 * std::atan2(ring.nodes[k].y, ring.nodes[k].x))};
+  DeformationConfig dc;
+  dc.greedy.tolerance = 0.1;
+  dc.greedy.max_levels = 3;
+  dc.greedy.basis = {WendlandKind::C2, 2.0};
+  dc.fixed_markers = {"far"};
+  const auto [deformed, report] = deform(ring, f, dc);
+  for (std::size_t k : outer.nodes) CHECK(deformed.nodes[k] == ring.nodes[k]);
+  CHECK(report.surface_max_error < 1e-3);
+  CHECK(!report.levels.empty() && report.total_control_points() > 0);
+  std::printf(failures ? "shim: %d FAILED\n" : "shim: all passed\n", failures);
+  return failures ? 1 : 0;
+}

@@ -61,3 +61,15 @@ def test_no_gpu_fails_loudly():
         pytest.skip("a GPU is present")
     with pytest.raises(RuntimeError):
         capi.Context(0)
+
+
+def test_cpp_api_shim_exports_reference_api():
+    """libicemorph_core.so implements the reference's public C++ API
+    (proj/include/icemorph) over the C-ABI."""
+    lib = os.path.join(ROOT, "paper_2107_13887_b200", "libicemorph_core.so")
+    out = subprocess.run(["nm", "-DC", "--defined-only", lib], capture_output=True, text=True).stdout
+    for sym in ("icemorph::deform(", "icemorph::update_volume(", "icemorph::build_distance_index(",
+                "icemorph::run_multilevel(", "icemorph::greedy_level(", "icemorph::solve_weights(",
+                "icemorph::eval_interpolant(", "icemorph::make_wall_function(",
+                "icemorph::eval_wendland("):
+        assert sym in out, sym

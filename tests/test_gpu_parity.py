@@ -340,3 +340,15 @@ def test_cfg2_full_selection(gpu):
     for l, lv in enumerate(m.levels):
         assert np.array_equal(lv.control_indices, ref[f"idx{l}"]), f"level {l}"
         assert lv.cap_hit == bool(ref["cap_hit"][l])
+
+
+def test_cpp_api_shim():
+    """The reference's public C++ API (icemorph/icemorph.hpp) backed by the
+    B200 library: the reference tests' known answers through the C++ shim."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "paper_2107_13887_b200", "build",
+                       "test_shim")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
