@@ -142,6 +142,25 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes,
                      im_basis basis, int precision, size_t* entry_nodes,
                      double* entry_values, size_t* n_entries);
 
+/* ---- element quality (the part deform reads) ----------------------------------
+ * signed_measures / count_inverted, quality.hpp (quality.cpp:100-148) on a
+ * mesh given as its node array (3 n_nodes doubles) and its volume elements in
+ * CSR form: element_kinds[n_elements] in ElementKind order (mesh.hpp:15-23:
+ * 0 line, 1 triangle, 2 quadrilateral, 3 tetrahedron, 4 hexahedron, 5 prism,
+ * 6 pyramid), element_offsets[n_elements + 1] (starting at 0) and
+ * element_nodes[element_offsets[n_elements]].  measures (nullable) receives
+ * n_elements doubles, *inverted (nullable) the count of measure <= 0.
+ * Malformed elements raise IM_INVALID_ARGUMENT with validate_mesh's message
+ * (mesh.cpp:168-185). */
+int im_signed_measures(im_context* ctx, const double* nodes, size_t n_nodes,
+                       const int* element_kinds, const size_t* element_offsets,
+                       const size_t* element_nodes, size_t n_elements, double* measures,
+                       size_t* inverted);
+/* count_inverted, quality.hpp (quality.cpp:142-148). */
+int im_count_inverted(im_context* ctx, const double* nodes, size_t n_nodes,
+                      const int* element_kinds, const size_t* element_offsets,
+                      const size_t* element_nodes, size_t n_elements, size_t* inverted);
+
 /* ---- pipeline -----------------------------------------------------------------
  * deform, pipeline.hpp:54-56 (pipeline.cpp:19-106) on a mesh given as its
  * node array and the node lists of the deforming patch and of the pinned
@@ -150,13 +169,21 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes,
  * support_distance < 0 selects the reference D_l = volume_k * target_max_l
  * (pipeline.cpp:66); >= 0 (inf allowed) is an absolute D (additive).
  * deformed_nodes: 3 n_nodes doubles.  Per-level outputs have max_levels
- * slots; quality metrics are out of scope (compute_quality = false). */
+ * slots.  When the config carries the mesh's volume elements (CSR as for
+ * im_signed_measures; n_elements = 0 for none) the report's
+ * inverted_elements is count_inverted(deformed) (pipeline.cpp:101),
+ * evaluated on the device-resident deformed nodes; the orthogonality
+ * quality report (compute_quality) is out of scope. */
 typedef struct {
   im_greedy_config greedy;
   double volume_k;
   double support_distance;
   int psi_kind;
   int precision;
+  const int* element_kinds;
+  const size_t* element_offsets;
+  const size_t* element_nodes;
+  size_t n_elements;
 } im_deform_config;
 
 typedef struct {
@@ -168,6 +195,7 @@ typedef struct {
   double greedy_seconds;
   double distance_seconds;
   double volume_seconds;
+  size_t inverted_elements;
 } im_deform_report;
 
 int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,

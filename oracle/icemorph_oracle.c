@@ -495,3 +495,60 @@ int or_update_volume(const double* nodes, size_t n_nodes, const double* dist,
   *out_n = k;
   return 0;
 }
+
+/* ---- quality.cpp:91-148 ---------------------------------------------------- */
+/* quality.cpp:91-93: dot(b - a, cross(c - a, d - a)) / 6, vec.hpp:51-55 order */
+static double tet_volume(const double* a, const double* b, const double* c, const double* d) {
+  const double u[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+  const double v[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+  const double w[3] = {d[0] - a[0], d[1] - a[1], d[2] - a[2]};
+  const double cx = v[1] * w[2] - v[2] * w[1];
+  const double cy = v[2] * w[0] - v[0] * w[2];
+  const double cz = v[0] * w[1] - v[1] * w[0];
+  return (u[0] * cx + u[1] * cy + u[2] * cz) / 6.0;
+}
+
+/* quality.cpp:95-97 */
+static double tri_area(const double* a, const double* b, const double* c) {
+  return 0.5 * ((b[0] - a[0]) * (c[1] - a[1]) - (c[0] - a[0]) * (b[1] - a[1]));
+}
+
+/* quality.cpp:101-133 */
+static double signed_measure(const double* nd, int kind, const size_t* n) {
+#define P(i) (nd + 3 * n[i])
+  switch (kind) {
+    case 1: return tri_area(P(0), P(1), P(2));
+    case 2: return tri_area(P(0), P(1), P(2)) + tri_area(P(0), P(2), P(3));
+    case 3: return tet_volume(P(0), P(1), P(2), P(3));
+    case 4: {
+      double v = 0.0;
+      v += tet_volume(P(0), P(1), P(2), P(6));
+      v += tet_volume(P(0), P(2), P(3), P(6));
+      v += tet_volume(P(0), P(3), P(7), P(6));
+      v += tet_volume(P(0), P(7), P(4), P(6));
+      v += tet_volume(P(0), P(4), P(5), P(6));
+      v += tet_volume(P(0), P(5), P(1), P(6));
+      return v;
+    }
+    case 5:
+      return tet_volume(P(0), P(1), P(2), P(3)) + tet_volume(P(1), P(2), P(3), P(4)) +
+             tet_volume(P(2), P(3), P(4), P(5));
+    case 6: return tet_volume(P(0), P(1), P(2), P(4)) + tet_volume(P(0), P(2), P(3), P(4));
+    default: return 0.0; /* Line */
+  }
+#undef P
+}
+
+int or_signed_measures(const double* nodes, size_t n_nodes, int dim, const int* kinds,
+                       const size_t* offsets, const size_t* conn, size_t n_elem, double* out,
+                       size_t* inverted) {
+  (void)n_nodes;
+  (void)dim;
+  size_t count = 0;
+  for (size_t e = 0; e < n_elem; ++e) {
+    out[e] = signed_measure(nodes, kinds[e], conn + offsets[e]);
+    if (out[e] <= 0.0) ++count; /* quality.cpp:145 */
+  }
+  *inverted = count;
+  return 0;
+}

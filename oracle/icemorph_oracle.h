@@ -72,6 +72,12 @@ int or_update_volume(const double* nodes, size_t n_nodes, const double* dist,
                      int psi_kind, int kind, double R, size_t* out_idx, double* out_val,
                      size_t* out_n, int nthreads);
 
+/* quality.cpp:91-148: signed element measures and the inverted count
+ * (measure <= 0).  kinds: mesh.hpp:15-23 order (0 Line .. 6 Pyramid), CSR. */
+int or_signed_measures(const double* nodes, size_t n_nodes, int dim, const int* kinds,
+                       const size_t* offsets, const size_t* conn, size_t n_elem, double* out,
+                       size_t* inverted);
+
 #ifdef __cplusplus
 }
 #endif

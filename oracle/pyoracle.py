@@ -238,9 +238,26 @@ class Oracle:
         k = cnt.value
         return idx[:k].astype(np.int64), val[:k].copy()
 
+    def signed_measures(self, nodes, dim, elements):
+        """quality.cpp:135-148: (measures, inverted) for a CSR element triple
+        (kinds int32, offsets uint64, conn uint64)."""
+        nodes = _xyz(nodes)
+        k, o, c = elements
+        k = np.ascontiguousarray(k, np.int32)
+        o = np.ascontiguousarray(o, np.uint64)
+        c = np.ascontiguousarray(c if len(c) else [0], np.uint64)
+        out = np.zeros(max(len(k), 1))
+        inv = _sz()
+        f = self._fn("signed_measures")
+        f.argtypes = [_pd, _sz, C.c_int, _pi, _psz, _psz, _sz, _pd, _psz]
+        self._check(f(_dp(nodes), len(nodes), dim, k.ctypes.data_as(_pi), _szp(o), _szp(c),
+                      len(k), _dp(out), C.byref(inv)))
+        return out[:len(k)].copy(), int(inv.value)
+
     def deform(self, nodes, dim, patch, disp, pinned=(), tol=0.1, max_levels=5, cap=5000,
-               kind="c2", R=1.0, volume_k=5.0):
-        """Reference deform() (ref flavour only)."""
+               kind="c2", R=1.0, volume_k=5.0, elements=None):
+        """Reference deform() (ref flavour only).  With ``elements`` (CSR
+        triple) the result carries ``inverted_elements`` (pipeline.cpp:101)."""
         assert self.flavour == "ref"
         nodes, disp = _xyz(nodes), _xyz(disp)
         patch = np.ascontiguousarray(patch, dtype=np.uint64)
@@ -252,17 +269,25 @@ class Oracle:
         caph = np.zeros(L, np.int32)
         nl = _sz()
         tmax, smax, smean, tsec = _d(), _d(), _d(), _d()
-        f = self.lib.ref_deform
+        if elements is None:
+            elements = (np.zeros(0, np.int32), np.zeros(1, np.uint64), np.zeros(1, np.uint64))
+        ek = np.ascontiguousarray(elements[0], np.int32)
+        eo = np.ascontiguousarray(elements[1], np.uint64)
+        ec = np.ascontiguousarray(elements[2] if len(elements[2]) else [0], np.uint64)
+        inv = _sz()
+        f = self.lib.ref_deform_elements
         f.argtypes = [_pd, _sz, C.c_int, _psz, _sz, _pd, _psz, _sz, _d, _sz, _sz, C.c_int, _d,
-                      _d, _pd, _psz, _psz, _psz, _pd, _pd, _pi, _pd, _pd, _pd, _pd]
+                      _d, _pd, _psz, _psz, _psz, _pd, _pd, _pi, _pd, _pd, _pd, _pd, _pi, _psz,
+                      _psz, _sz, _psz]
         self._check(f(_dp(nodes), len(nodes), dim, _szp(patch), len(patch), _dp(disp),
                       _szp(pinned) if len(pinned) else None, len(pinned), tol, max_levels, cap,
                       KINDS.get(kind, kind), R, volume_k, _dp(out), C.byref(nl), _szp(pts),
                       _szp(tch), _dp(sup), _dp(ach), caph.ctypes.data_as(_pi), C.byref(tmax),
-                      C.byref(smax), C.byref(smean), C.byref(tsec)))
+                      C.byref(smax), C.byref(smean), C.byref(tsec), ek.ctypes.data_as(_pi),
+                      _szp(eo), _szp(ec), len(ek), C.byref(inv)))
         k = nl.value
         return dict(nodes=out, points=pts[:k].astype(np.int64), touched=tch[:k].astype(np.int64),
                     support=sup[:k].copy(), achieved=ach[:k].copy(),
                     cap_hit=caph[:k].astype(bool), target_max=tmax.value,
                     surface_max_error=smax.value, surface_mean_error=smean.value,
-                    total_seconds=tsec.value)
+                    total_seconds=tsec.value, inverted_elements=int(inv.value))

@@ -14,6 +14,8 @@
 //   ref_build_distance_index -> build_distance_index     (wall_distance.cpp:13-31)
 //   ref_update_volume        -> update_volume            (wall_distance.cpp:46-64)
 //   ref_deform               -> deform                   (pipeline.cpp:19-106)
+//   ref_deform_elements      -> deform with volume elements (report.inverted_elements)
+//   ref_signed_measures      -> signed_measures / count_inverted (quality.cpp:135-148)
 //
 // The psi = Wendland-C2 taper (BASELINE cfg1 "psi = Wendland C2 of xi") has
 // no reference implementation; for psi_kind == 1 ref_update_volume restates
@@ -37,6 +39,7 @@
 
 #include "icemorph/greedy.hpp"
 #include "icemorph/pipeline.hpp"
+#include "icemorph/quality.hpp"
 #include "icemorph/rbf.hpp"
 #include "icemorph/wall_distance.hpp"
 
@@ -273,22 +276,29 @@ int ref_update_volume(const double* nodes, size_t n_nodes, const double* dist,
   });
 }
 
-// deform() on a mesh given as node array + marker node lists (no elements, so
-// count_inverted is 0 and compute_quality must be false).  marker 0 is the
+// deform() on a mesh given as node array + marker node lists (+ optional
+// volume elements for report.inverted_elements; compute_quality is false).  marker 0 is the
 // deforming patch; markers 1.. are pinned.  disp holds one displacement per
 // node of marker 0 (same order).  Outputs: deformed node array, per-level
 // (points, touched, support_distance, achieved, cap_hit), surface errors.
-int ref_deform(const double* nodes, size_t n_nodes, int dim, const size_t* patch,
-               size_t n_patch, const double* disp, const size_t* pinned, size_t n_pinned,
-               double tol, size_t max_levels, size_t cap, int kind, double R, double volume_k,
-               double* out_nodes, size_t* out_nlevels, size_t* out_points,
-               size_t* out_touched, double* out_support, double* out_achieved,
-               int* out_cap_hit, double* out_target_max, double* out_surface_max,
-               double* out_surface_mean, double* out_total_seconds) {
+static int deform_impl(const double* nodes, size_t n_nodes, int dim, const size_t* patch,
+                       size_t n_patch, const double* disp, const size_t* pinned, size_t n_pinned,
+                       double tol, size_t max_levels, size_t cap, int kind, double R,
+                       double volume_k, double* out_nodes, size_t* out_nlevels, size_t* out_points,
+                       size_t* out_touched, double* out_support, double* out_achieved,
+                       int* out_cap_hit, double* out_target_max, double* out_surface_max,
+                       double* out_surface_mean, double* out_total_seconds, const int* kinds,
+                       const size_t* offsets, const size_t* conn, size_t n_elem,
+                       size_t* out_inverted) {
   return guarded([&] {
     Mesh mesh;
     mesh.dim = dim;
     mesh.nodes = to_vecs(nodes, n_nodes);
+    mesh.elements.resize(n_elem);
+    for (size_t e = 0; e < n_elem; ++e) {
+      mesh.elements[e].kind = static_cast<ElementKind>(kinds[e]);
+      mesh.elements[e].nodes.assign(conn + offsets[e], conn + offsets[e + 1]);
+    }
     Marker m;
     m.name = "patch";
     m.nodes.assign(patch, patch + n_patch);
@@ -322,7 +332,68 @@ int ref_deform(const double* nodes, size_t n_nodes, int dim, const size_t* patch
     *out_surface_max = rep.surface_max_error;
     *out_surface_mean = rep.surface_mean_error;
     *out_total_seconds = rep.total_seconds;
+    if (out_inverted) *out_inverted = rep.inverted_elements;  // pipeline.cpp:101
   });
 }
 
+int ref_deform(const double* nodes, size_t n_nodes, int dim, const size_t* patch,
+               size_t n_patch, const double* disp, const size_t* pinned, size_t n_pinned,
+               double tol, size_t max_levels, size_t cap, int kind, double R, double volume_k,
+               double* out_nodes, size_t* out_nlevels, size_t* out_points,
+               size_t* out_touched, double* out_support, double* out_achieved,
+               int* out_cap_hit, double* out_target_max, double* out_surface_max,
+               double* out_surface_mean, double* out_total_seconds) {
+  return deform_impl(nodes, n_nodes, dim, patch, n_patch, disp, pinned, n_pinned, tol, max_levels,
+                     cap, kind, R, volume_k, out_nodes, out_nlevels, out_points, out_touched,
+                     out_support, out_achieved, out_cap_hit, out_target_max, out_surface_max,
+                     out_surface_mean, out_total_seconds, nullptr, nullptr, nullptr, 0, nullptr);
+}
+
+// deform on a mesh that carries its volume elements; *out_inverted receives
+// report.inverted_elements = count_inverted(deformed) (pipeline.cpp:101).
+int ref_deform_elements(const double* nodes, size_t n_nodes, int dim, const size_t* patch,
+                        size_t n_patch, const double* disp, const size_t* pinned,
+                        size_t n_pinned, double tol, size_t max_levels, size_t cap, int kind,
+                        double R, double volume_k, double* out_nodes, size_t* out_nlevels,
+                        size_t* out_points, size_t* out_touched, double* out_support,
+                        double* out_achieved, int* out_cap_hit, double* out_target_max,
+                        double* out_surface_max, double* out_surface_mean,
+                        double* out_total_seconds, const int* kinds, const size_t* offsets,
+                        const size_t* conn, size_t n_elem, size_t* out_inverted) {
+  return deform_impl(nodes, n_nodes, dim, patch, n_patch, disp, pinned, n_pinned, tol, max_levels,
+                     cap, kind, R, volume_k, out_nodes, out_nlevels, out_points, out_touched,
+                     out_support, out_achieved, out_cap_hit, out_target_max, out_surface_max,
+                     out_surface_mean, out_total_seconds, kinds, offsets, conn, n_elem,
+                     out_inverted);
+}
+
 }  // extern "C"
+
+// ---- quality: signed_measures / count_inverted ------
+// Element kinds follow mesh.hpp:15-23 (0 Line, 1 Triangle, 2 Quadrilateral,
+// 3 Tetrahedron, 4 Hexahedron, 5 Prism, 6 Pyramid); CSR connectivity.
+namespace {
+Mesh mesh_with_elements(const double* nodes, size_t n_nodes, int dim, const int* kinds,
+                        const size_t* offsets, const size_t* conn, size_t n_elem) {
+  Mesh m;
+  m.dim = dim;
+  m.nodes = to_vecs(nodes, n_nodes);
+  m.elements.resize(n_elem);
+  for (size_t e = 0; e < n_elem; ++e) {
+    m.elements[e].kind = static_cast<ElementKind>(kinds[e]);
+    m.elements[e].nodes.assign(conn + offsets[e], conn + offsets[e + 1]);
+  }
+  return m;
+}
+}  // namespace
+
+extern "C" int ref_signed_measures(const double* nodes, size_t n_nodes, int dim, const int* kinds,
+                                   const size_t* offsets, const size_t* conn, size_t n_elem,
+                                   double* out, size_t* inverted) {
+  return guarded([&] {
+    const Mesh m = mesh_with_elements(nodes, n_nodes, dim, kinds, offsets, conn, n_elem);
+    const std::vector<double> v = signed_measures(m);  // quality.cpp:135-140
+    std::memcpy(out, v.data(), n_elem * sizeof(double));
+    *inverted = count_inverted(m);  // quality.cpp:142-148
+  });
+}

@@ -55,14 +55,17 @@ class WallFunctionC(C.Structure):
 
 class DeformConfigC(C.Structure):
     _fields_ = [("greedy", GreedyConfigC), ("volume_k", C.c_double),
-                ("support_distance", C.c_double), ("psi_kind", C.c_int), ("precision", C.c_int)]
+                ("support_distance", C.c_double), ("psi_kind", C.c_int), ("precision", C.c_int),
+                ("element_kinds", C.POINTER(C.c_int)), ("element_offsets", C.POINTER(C.c_size_t)),
+                ("element_nodes", C.POINTER(C.c_size_t)), ("n_elements", C.c_size_t)]
 
 
 class DeformReportC(C.Structure):
     _fields_ = [("n_levels", C.c_size_t), ("target_max", C.c_double),
                 ("surface_max_error", C.c_double), ("surface_mean_error", C.c_double),
                 ("total_seconds", C.c_double), ("greedy_seconds", C.c_double),
-                ("distance_seconds", C.c_double), ("volume_seconds", C.c_double)]
+                ("distance_seconds", C.c_double), ("volume_seconds", C.c_double),
+                ("inverted_elements", C.c_size_t)]
 
 
 _lib = None
@@ -88,7 +91,7 @@ EXPORTS = [
     "im_context_create", "im_context_destroy", "im_last_error", "im_last_device_ms",
     "im_version", "im_eval_wendland", "im_eval_basis", "im_make_wall_function",
     "im_eval_wall_function", "im_solve_weights", "im_eval_interpolant", "im_greedy_level",
-    "im_run_multilevel", "im_build_distance_index", "im_update_volume", "im_deform",
+    "im_run_multilevel", "im_build_distance_index", "im_signed_measures", "im_count_inverted", "im_update_volume", "im_deform",
     "im_volume_plan_create", "im_volume_plan_destroy", "im_volume_plan_set_controls",
     "im_volume_plan_run", "im_volume_plan_reset_field", "im_volume_plan_download_field",
     "im_volume_plan_distances", "im_volume_plan_set_level", "im_volume_plan_run_steps",
@@ -118,6 +121,8 @@ def _declare(L):
     L.im_run_multilevel.argtypes = [C.c_void_p, _pd, _pd, _sz, C.POINTER(GreedyConfigC), _psz,
                                     _psz, _psz, _pd, _pd, _pi, _pd, _pd, _psz, _pd, _pd, _pd]
     L.im_build_distance_index.argtypes = [C.c_void_p, _pd, _sz, C.c_int, _psz, _sz, _pd]
+    L.im_signed_measures.argtypes = [C.c_void_p, _pd, _sz, _pi, _psz, _psz, _sz, _pd, _psz]
+    L.im_count_inverted.argtypes = [C.c_void_p, _pd, _sz, _pi, _psz, _psz, _sz, _psz]
     L.im_update_volume.argtypes = [C.c_void_p, _pd, _sz, _pd, _pd, _pd, _sz,
                                    C.POINTER(WallFunctionC), Basis, C.c_int, _psz, _pd, _psz]
     L.im_deform.argtypes = [C.c_void_p, _pd, _sz, C.c_int, _psz, _sz, _pd, _psz, _sz,
@@ -330,14 +335,41 @@ class Context:
         k = cnt.value
         return idx[:k].astype(np.int64), val[:k].copy()
 
+    def signed_measures(self, nodes, elements):
+        """quality.cpp:135-148: (measures, inverted) for ``elements`` =
+        (kinds, offsets, conn) CSR (see :func:`elements_csr`)."""
+        nodes = xyz(nodes)
+        k, o, c = elements
+        m = np.zeros(max(len(k), 1))
+        inv = _sz()
+        self._check(self.lib.im_signed_measures(
+            self.h, _dp(nodes), len(nodes), k.ctypes.data_as(_pi), _szp(o), _szp(c), len(k),
+            _dp(m), C.byref(inv)))
+        return m[:len(k)].copy(), int(inv.value)
+
+    def count_inverted(self, nodes, elements) -> int:
+        nodes = xyz(nodes)
+        k, o, c = elements
+        inv = _sz()
+        self._check(self.lib.im_count_inverted(
+            self.h, _dp(nodes), len(nodes), k.ctypes.data_as(_pi), _szp(o), _szp(c), len(k),
+            C.byref(inv)))
+        return int(inv.value)
+
     def deform(self, nodes, dim, patch, disp, pinned=(), tol=0.1, max_levels=5, cap=5000,
                kind="c2", R=1.0, volume_k=5.0, support_distance=-1.0, psi_kind=0,
-               precision=FP64):
+               precision=FP64, elements=None):
         nodes, disp = xyz(nodes), xyz(disp)
         patch = np.ascontiguousarray(patch, dtype=np.uint64)
         pinned = np.ascontiguousarray(np.asarray(pinned, dtype=np.uint64).reshape(-1))
         cfg = DeformConfigC(GreedyConfigC(tol, max_levels, cap, basis(kind, R)), volume_k,
                             support_distance, psi_kind, precision)
+        if elements is not None and len(elements[0]):
+            ek, eo, ec = elements
+            cfg.element_kinds = ek.ctypes.data_as(_pi)
+            cfg.element_offsets = _szp(eo)
+            cfg.element_nodes = _szp(ec)
+            cfg.n_elements = len(ek)
         rep = DeformReportC()
         out = np.zeros_like(nodes)
         L = max_levels
@@ -356,7 +388,28 @@ class Context:
                     target_max=rep.target_max, surface_max_error=rep.surface_max_error,
                     surface_mean_error=rep.surface_mean_error, total_seconds=rep.total_seconds,
                     greedy_seconds=rep.greedy_seconds, distance_seconds=rep.distance_seconds,
-                    volume_seconds=rep.volume_seconds)
+                    volume_seconds=rep.volume_seconds, inverted_elements=rep.inverted_elements)
+
+
+ELEMENT_KINDS = ("line", "triangle", "quadrilateral", "tetrahedron", "hexahedron", "prism",
+                 "pyramid")  # mesh.hpp:15-23 order
+
+
+def elements_csr(elements):
+    """Element list -> (kinds int32, offsets uint64, conn uint64) CSR.  Accepts
+    a list of (kind, nodes) pairs (kind an int or an ELEMENT_KINDS name) or an
+    already-built CSR triple."""
+    if isinstance(elements, tuple) and len(elements) == 3 and isinstance(elements[0], np.ndarray):
+        k, o, c = elements
+        return (np.ascontiguousarray(k, np.int32), np.ascontiguousarray(o, np.uint64),
+                np.ascontiguousarray(c, np.uint64))
+    kinds, offs, conn = [], [0], []
+    for kind, nodes in elements:
+        kinds.append(ELEMENT_KINDS.index(kind) if isinstance(kind, str) else int(kind))
+        conn.extend(int(i) for i in nodes)
+        offs.append(len(conn))
+    return (np.asarray(kinds, np.int32), np.asarray(offs, np.uint64),
+            np.asarray(conn if conn else [0], np.uint64))
 
 
 class VolumePlan:

@@ -8,8 +8,9 @@
 //
 // Additive fields (defaults reproduce the reference): WallFunction::psi_kind,
 // DeformationConfig::{support_distance, psi_kind, precision}.  Out of scope
-// (not on the hot path): mesh I/O, generators, quality metrics; DeformationReport
-// carries no quality reports (compute_quality is accepted and ignored).
+// (not on the hot path): mesh I/O, generators, the orthogonality report;
+// DeformationReport carries inverted_elements but no QualityReport
+// (compute_quality is accepted and ignored).
 #pragma once
 
 #include <cmath>
@@ -200,6 +201,11 @@ struct DeformationReport {
 std::pair<Mesh, DeformationReport> deform(const Mesh& mesh, const DisplacementField& displacement,
                                           const DeformationConfig& config);
 void write_summary(const DeformationReport& report, std::ostream& out);
+
+// ---- quality.hpp: the measures deform's report reads (device-evaluated) ------------
+std::vector<double> signed_measures(const Mesh& mesh);
+double signed_measure(const Mesh& mesh, const Element& element);
+std::size_t count_inverted(const Mesh& mesh);
 void write_convergence_csv(const DeformationReport& report, std::ostream& out);
 
 }  // namespace icemorph

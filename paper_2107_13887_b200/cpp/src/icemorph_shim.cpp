@@ -228,6 +228,46 @@ std::size_t DeformationReport::total_control_points() const {
   return t;
 }
 
+namespace {
+// Mesh::elements -> the C-ABI's CSR element arrays.
+struct ElementCsr {
+  std::vector<int> kinds;
+  std::vector<std::size_t> offsets{0}, nodes;
+  explicit ElementCsr(const std::vector<Element>& elements) {
+    kinds.reserve(elements.size());
+    offsets.reserve(elements.size() + 1);
+    for (const auto& e : elements) {
+      kinds.push_back(static_cast<int>(e.kind));
+      nodes.insert(nodes.end(), e.nodes.begin(), e.nodes.end());
+      offsets.push_back(nodes.size());
+    }
+  }
+  const std::size_t* conn() const { return nodes.empty() ? offsets.data() : nodes.data(); }
+};
+
+std::size_t measures(const Mesh& mesh, const std::vector<Element>& elements, double* out) {
+  const ElementCsr csr(elements);
+  std::size_t inverted = 0;
+  check(im_signed_measures(ctx(), xyz(mesh.nodes), mesh.nodes.size(), csr.kinds.data(),
+                           csr.offsets.data(), csr.conn(), elements.size(), out, &inverted));
+  return inverted;
+}
+}  // namespace
+
+std::vector<double> signed_measures(const Mesh& mesh) {
+  std::vector<double> m(mesh.elements.size());
+  measures(mesh, mesh.elements, m.data());
+  return m;
+}
+
+double signed_measure(const Mesh& mesh, const Element& element) {
+  double m = 0.0;
+  measures(mesh, {element}, &m);
+  return m;
+}
+
+std::size_t count_inverted(const Mesh& mesh) { return measures(mesh, mesh.elements, nullptr); }
+
 std::pair<Mesh, DeformationReport> deform(const Mesh& mesh, const DisplacementField& disp,
                                           const DeformationConfig& config) {
   const Marker& marker = mesh.marker(disp.patch);
@@ -238,8 +278,10 @@ std::pair<Mesh, DeformationReport> deform(const Mesh& mesh, const DisplacementFi
     for (std::size_t n : mesh.marker(name).nodes) pinned.push_back(n);
   std::vector<Vec3> d(marker.nodes.size());
   for (std::size_t i = 0; i < marker.nodes.size(); ++i) d[i] = disp.at(marker.nodes[i]);
+  const ElementCsr csr(mesh.elements);
   const im_deform_config cfg{to_c(config.greedy), config.volume_k, config.support_distance,
-                             config.psi_kind, config.precision};
+                             config.psi_kind,      config.precision, csr.kinds.data(),
+                             csr.offsets.data(),   csr.conn(),       mesh.elements.size()};
   Mesh out = mesh;
   im_deform_report rep{};
   const std::size_t L = std::max<std::size_t>(1, config.greedy.max_levels);
@@ -266,6 +308,7 @@ std::pair<Mesh, DeformationReport> deform(const Mesh& mesh, const DisplacementFi
   r.target_max = rep.target_max;
   r.surface_max_error = rep.surface_max_error;
   r.surface_mean_error = rep.surface_mean_error;
+  r.inverted_elements = rep.inverted_elements;
   r.total_seconds = rep.total_seconds;
   return {std::move(out), std::move(r)};
 }

@@ -379,6 +379,26 @@ int im_run_multilevel(im_context* ctx, const double* pos, const double* target, 
   });
 }
 
+int im_signed_measures(im_context* ctx, const double* nodes, size_t n_nodes, const int* kinds,
+                       const size_t* offsets, const size_t* conn, size_t n_elem, double* measures,
+                       size_t* inverted) {
+  return guarded(ctx, [&](Context& c) {
+    DPoints dn;
+    upload_points(c, nodes, n_nodes, dn);
+    EventTimer tm(c.stream);
+    const size_t k =
+        signed_measures_from_host(c, dn.x.p, dn.y.p, dn.z.p, n_nodes, kinds, offsets, conn, n_elem,
+                                  measures);
+    c.last_kernel_ms = tm.stop();
+    if (inverted) *inverted = k;
+  });
+}
+
+int im_count_inverted(im_context* ctx, const double* nodes, size_t n_nodes, const int* kinds,
+                      const size_t* offsets, const size_t* conn, size_t n_elem, size_t* inverted) {
+  return im_signed_measures(ctx, nodes, n_nodes, kinds, offsets, conn, n_elem, nullptr, inverted);
+}
+
 int im_build_distance_index(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
                             const size_t* surface, size_t n_surface, double* out) {
   return guarded(ctx, [&](Context& c) {

@@ -349,6 +349,12 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
       if (level_seconds) level_seconds[l] = lv.seconds;
     }
     c.last_kernel_ms = tm.ms();
+    // count_inverted(deformed) (pipeline.cpp:101) on the resident deformed nodes
+    rep->inverted_elements = 0;
+    if (cfg->n_elements)
+      rep->inverted_elements = signed_measures_from_host(
+          c, acc.x.p, acc.y.p, acc.z.p, n_nodes, cfg->element_kinds, cfg->element_offsets,
+          cfg->element_nodes, cfg->n_elements, nullptr);
     DBuf<double> aos;
     aos.reserve(3 * n_nodes);
     k_soa_to_aos<<<(n_nodes + 255) / 256, 256, 0, c.stream>>>(acc.x.p, acc.y.p, acc.z.p, n_nodes,

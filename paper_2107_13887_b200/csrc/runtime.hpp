@@ -118,7 +118,7 @@ struct Context {
   enum Slot : int {
     kSlotNodesX, kSlotNodesY, kSlotNodesZ, kSlotDist, kSlotActive, kSlotPerm, kSlotVals,
     kSlotTiles, kSlotBoxes, kSlotStage, kSlotCell, kSlotCounts, kSlotStart, kSlotBox,
-    kSlotScanA, kSlotScanB, kSlotCount
+    kSlotScanA, kSlotScanB, kSlotElemKind, kSlotElemOffset, kSlotElemNodes, kSlotCount
   };
   DBuf<unsigned char> slots[kSlotCount];
   template <class T>
@@ -211,6 +211,16 @@ void scan_u32_to_u64(Context& ctx, const unsigned int* in, size_t n, unsigned lo
 // Exact wall distance (wall_distance.cpp:13-31).  cutoff = +inf for exact
 // distances everywhere; a finite cutoff lets the search stop once no surface
 // point can lie closer than cutoff (such nodes get +inf, i.e. inactive).
+// quality.cpp:135-148 on the device: signed measure of every element (out may
+// be null) and the number with measure <= 0.  Element arrays are device CSR.
+size_t signed_measures(Context& ctx, const double* x, const double* y, const double* z,
+                       size_t n_nodes, const int* kinds, const unsigned long long* offsets,
+                       const unsigned long long* conn, size_t n_elem, double* out);
+// Same with the element CSR (and out) on the host; uploads through context slots.
+size_t signed_measures_from_host(Context& ctx, const double* x, const double* y, const double* z,
+                                 size_t n_nodes, const int* kinds, const size_t* offsets,
+                                 const size_t* conn, size_t n_elem, double* out);
+
 void wall_distance(Context& ctx, const DPoints& nodes, size_t n_nodes, const DPoints& surface,
                    size_t n_surface, int dim, double cutoff, double* d_out);
 

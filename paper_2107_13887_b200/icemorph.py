@@ -7,9 +7,11 @@ Same names, argument meaning and error behaviour as the reference binding:
 ``Mesh`` / ``DisplacementField`` / ``DeformationConfig`` / ``DeformationReport``
 / ``LevelSummary``; ``ValueError`` for std::invalid_argument and
 ``RuntimeError`` (``capi.SolveError``) for icemorph::SolveError, as pybind11
-maps them.  Mesh I/O, generators and quality metrics are out of scope; a
-``Mesh`` is built from arrays (``Mesh(dim, nodes, markers)``) instead of
-``read_su2`` / ``gen_airfoil_mesh``.
+maps them, plus ``signed_measures`` (bindings.cpp:195-197) and the report's
+``inverted_elements`` (pipeline.cpp:101) on the device.  Mesh I/O, generators
+and the orthogonality report are out of scope; a ``Mesh`` is built from
+arrays (``Mesh(dim, nodes, markers, elements)``) instead of ``read_su2`` /
+``gen_airfoil_mesh``.
 """
 from __future__ import annotations
 
@@ -55,17 +57,24 @@ def eval_interpolant(points, alpha, kind, support_radius, query):
 
 
 class Mesh:
-    """Node array + named markers (the part of the reference Mesh the hot path
-    reads, mesh.hpp:42-58)."""
+    """Node array + named markers + volume elements (the part of the reference
+    Mesh the hot path reads, mesh.hpp:42-58).  ``elements``: list of
+    (kind, node list) with kind an ElementKind index or name
+    (``capi.ELEMENT_KINDS``), or a CSR triple from ``capi.elements_csr``."""
 
-    def __init__(self, dim: int, nodes, markers: dict):
+    def __init__(self, dim: int, nodes, markers: dict, elements=()):
         self.dim = int(dim)
         self._nodes = capi.xyz(nodes)
         self._markers = {k: [int(i) for i in v] for k, v in markers.items()}
+        self._elements = capi.elements_csr(elements)
 
     @property
     def num_nodes(self) -> int:
         return len(self._nodes)
+
+    @property
+    def num_elements(self) -> int:
+        return len(self._elements[0])
 
     def node(self, i):
         if not 0 <= i < len(self._nodes):
@@ -152,6 +161,16 @@ class DeformationReport:
         return sum(l.points for l in self.levels)
 
 
+def signed_measures(mesh: Mesh):
+    """bindings.cpp:195-197 -> signed_measures (quality.cpp:135-140)."""
+    return _context().signed_measures(mesh._nodes, mesh._elements)[0].tolist()
+
+
+def count_inverted(mesh: Mesh) -> int:
+    """count_inverted (quality.cpp:142-148)."""
+    return _context().count_inverted(mesh._nodes, mesh._elements)
+
+
 def deform(mesh: Mesh, displacement: DisplacementField, config: DeformationConfig):
     """bindings.cpp:191-193 -> deform (pipeline.cpp:19-106).  Returns
     (deformed_mesh, report); the input mesh is left unchanged."""
@@ -165,11 +184,13 @@ def deform(mesh: Mesh, displacement: DisplacementField, config: DeformationConfi
                           config.levels, config.max_points_per_level, _kind(config.basis),
                           config.support_radius, config.volume_k, D,
                           1 if config.psi in ("c2", "wendland_c2") else 0,
-                          capi.EXACT if config.precision == "exact" else capi.FP64)
-    out = Mesh(mesh.dim, r["nodes"], mesh._markers)
+                          capi.EXACT if config.precision == "exact" else capi.FP64,
+                          elements=mesh._elements)
+    out = Mesh(mesh.dim, r["nodes"], mesh._markers, mesh._elements)
     rep = DeformationReport(marker=displacement.patch, target_max=r["target_max"],
                             surface_max_error=r["surface_max_error"],
                             surface_mean_error=r["surface_mean_error"],
+                            inverted_elements=int(r["inverted_elements"]),
                             total_seconds=r["total_seconds"])
     for l in range(len(r["points"])):
         rep.levels.append(LevelSummary(l, int(r["points"][l]), float(r["achieved"][l]),

@@ -134,7 +134,8 @@ def _airfoil_case(name, n_surf, ring, layers, bump, R, tol, levels, D, psi_kind,
     s = arc_from_le(surf)
     disp = bump(s)[:, None] * outward_normals_2d(surf)
     return Workload(name, 2, np.ascontiguousarray(nodes), surface, np.ascontiguousarray(disp),
-                    R, tol, levels, D, psi_kind, meta=dict(seed=seed, ring=ring, layers=layers))
+                    R, tol, levels, D, psi_kind,
+                    meta=dict(seed=seed, ring=ring, layers=layers, n_volume=len(vol)))
 
 
 def cfg1(scale: float = 1.0) -> Workload:
@@ -206,7 +207,9 @@ def _wing_case(name, n_chord, n_span, vol_around, vol_span, layers, first, disp_
     surface = np.arange(len(vol), len(nodes), dtype=np.int64)
     disp = disp_fn(spts, prof, np.random.default_rng(seed)).reshape(-1, 3)
     return Workload(name, 3, np.ascontiguousarray(nodes), surface, np.ascontiguousarray(disp),
-                    R, tol, levels, D, 0, meta=dict(seed=seed))
+                    R, tol, levels, D, 0,
+                    meta=dict(seed=seed, around=vol_around, span=vol_span, layers=layers,
+                              n_volume=len(vol)))
 
 
 def _ridge(spts, prof, rng):
@@ -254,6 +257,60 @@ def cfg4(scale: float = 1.0) -> Workload:
     s = scale
     return _wing_case("cfg4_3d_global_wing", int(500 * s), int(200 * s), int(400 * s),
                       int(2000 * s), 50, 0.0349, _bend_twist, 40.0, 1e-4, 4, math.inf, 4)
+
+
+# ---- volume elements (for count_inverted, quality.cpp:142-148) -------------
+# ElementKind ids (mesh.hpp:15-23)
+QUAD, HEX = 2, 4
+
+
+def _csr(kind: int, conn: np.ndarray):
+    n, k = conn.shape
+    return (np.full(n, kind, np.int32), np.arange(0, (n + 1) * k, k, dtype=np.uint64),
+            np.ascontiguousarray(conn.reshape(-1), dtype=np.uint64))
+
+
+def o_mesh_elements(ring: int, layers: int, nodes: np.ndarray | None = None):
+    """Quadrilaterals of the O-mesh (node l*ring + i), wrapping around the ring,
+    oriented so the undeformed cells have positive area (checked on ``nodes``
+    when given)."""
+    l, i = np.meshgrid(np.arange(layers - 1), np.arange(ring), indexing="ij")
+    l, i = l.reshape(-1), i.reshape(-1)
+    i1 = (i + 1) % ring
+    conn = np.stack([l * ring + i, l * ring + i1, (l + 1) * ring + i1, (l + 1) * ring + i], 1)
+    if nodes is not None:
+        a, b, c = nodes[conn[0, 0]], nodes[conn[0, 1]], nodes[conn[0, 2]]
+        if (b[0] - a[0]) * (c[1] - a[1]) - (c[0] - a[0]) * (b[1] - a[1]) < 0:
+            conn = conn[:, [0, 3, 2, 1]]
+    return _csr(QUAD, conn)
+
+
+def wing_volume_elements(n_around: int, n_span: int, layers: int,
+                         nodes: np.ndarray | None = None):
+    """Hexahedra of the wing volume (node (l*n_span + j)*n_around + i),
+    wrapping around the section; oriented to positive volume."""
+    l, j, i = np.meshgrid(np.arange(layers - 1), np.arange(n_span - 1), np.arange(n_around),
+                          indexing="ij")
+    l, j, i = l.reshape(-1), j.reshape(-1), i.reshape(-1)
+    i1 = (i + 1) % n_around
+    idx = lambda ll, jj, ii: (ll * n_span + jj) * n_around + ii
+    conn = np.stack([idx(l, j, i), idx(l, j, i1), idx(l, j + 1, i1), idx(l, j + 1, i),
+                     idx(l + 1, j, i), idx(l + 1, j, i1), idx(l + 1, j + 1, i1),
+                     idx(l + 1, j + 1, i)], 1)
+    if nodes is not None:
+        p = nodes[conn[0]]
+        u, v, w = p[1] - p[0], p[3] - p[0], p[4] - p[0]
+        if np.dot(u, np.cross(v, w)) < 0:
+            conn = conn[:, [0, 3, 2, 1, 4, 7, 6, 5]]
+    return _csr(HEX, conn)
+
+
+def elements(w: Workload):
+    """CSR volume elements (kinds, offsets, conn) of a cfg workload's mesh."""
+    m = w.meta
+    if w.dim == 2:
+        return o_mesh_elements(m["ring"], m["layers"], w.nodes)
+    return wing_volume_elements(m["around"], m["span"], m["layers"], w.nodes)
 
 
 def raw(n_ctrl: int, n_vol: int, R: float, D: float = math.inf, seed: int = 5,

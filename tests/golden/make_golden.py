@@ -22,6 +22,9 @@ from pyoracle import Oracle  # noqa: E402
 
 from paper_2107_13887_b200 import workloads as W  # noqa: E402
 
+sys.path.insert(0, os.path.dirname(HERE))
+import meshes as M  # noqa: E402
+
 
 def random_cloud(rng, n, dim, min_sep):
     """Rejection-sampled cloud with a minimum separation (test_rbf.cpp:13-30)."""
@@ -96,6 +99,16 @@ def main():
     out["cfg1s_nodes"], out["cfg1s_surface"], out["cfg1s_disp"] = w.nodes, w.surface, w.displacement
     out["cfg1s_deformed"] = r["nodes"]
     out["cfg1s_touched"] = r["touched"]
+    # quality (quality.cpp:135-148): random mixed elements, about half inverted
+    nodes, (k, o, c) = M.random_mixed(np.random.default_rng(11), 400, 3000)
+    meas, inv = ref.signed_measures(nodes, 3, (k, o, c))
+    out.update(q_nodes=nodes, q_kinds=k, q_offsets=o, q_conn=c, q_measures=meas,
+               q_inverted=np.array(inv))
+    # test_pipeline.cpp:216-228: a tall bump through a shallow quad grid inverts cells
+    nodes, el, wall = M.quad_grid(10, 3, 1.0, 0.05)
+    disp = M.wall_bump(nodes, wall, 0.5)
+    r = ref.deform(nodes, 2, wall, disp, (), 0.01, 2, 5000, "c2", 0.3, 0.2, elements=el)
+    out.update(inv_deformed=r["nodes"], inv_count=np.array(r["inverted_elements"]))
     np.savez_compressed(os.path.join(HERE, "reference_outputs.npz"), **out)
     print("wrote", len(out), "arrays")
 
