@@ -325,15 +325,16 @@ class Context:
         if len(dist) != len(nodes):
             raise ValueError("distance index does not match the mesh")
         n = len(nodes)
-        idx = np.zeros(max(n, 1), np.uint64)
-        val = np.zeros((max(n, 1), 3))
+        idx = np.empty(max(n, 1), np.uint64)
+        val = np.empty((max(n, 1), 3))
         cnt = _sz()
         wf = WallFunctionC(1.0, D, psi_kind)
         self._check(self.lib.im_update_volume(self.h, _dp(nodes), n, _dp(dist), _dp(c), _dp(a),
                                               len(c), C.byref(wf), basis(kind, R), precision,
                                               _szp(idx), _dp(val), C.byref(cnt)))
         k = cnt.value
-        return idx[:k].astype(np.int64), val[:k].copy()
+        # views of the output buffers (no copy): node ids as int64, values (k, 3)
+        return idx[:k].view(np.int64), val[:k]
 
     def signed_measures(self, nodes, elements):
         """quality.cpp:135-148: (measures, inverted) for ``elements`` =

@@ -6,8 +6,11 @@
 // (max_magnitude, the SolveError distances, the surface error) is compiled
 // with -ffp-contract=off and follows the cited reference lines.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -16,6 +19,7 @@
 
 #include "../../include/icemorph_b200.h"
 #include "greedy.hpp"
+#include "host_io.hpp"
 #include "runtime.hpp"
 
 namespace imb {
@@ -130,6 +134,23 @@ int guarded(im_context* ctx, F&& f) {
   }
   return c.status;
 }
+
+// IMB_TRACE=1: per-phase host wall times of a C-ABI call on stderr (each mark
+// synchronises the stream, so only for diagnosis).
+struct PhaseTrace {
+  cudaStream_t s;
+  bool on;
+  Clock::time_point t;
+  explicit PhaseTrace(cudaStream_t st) : s(st), on(std::getenv("IMB_TRACE") != nullptr), t(Clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto n = Clock::now();
+    std::fprintf(stderr, "[imb] %-28s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
 
 struct EventTimer {
   cudaEvent_t a, b;
@@ -424,6 +445,7 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
                      const im_wall_function* wf, im_basis basis, int precision,
                      size_t* entry_nodes, double* entry_values, size_t* n_entries) {
   return guarded(ctx, [&](Context& c) {
+    PhaseTrace tr(c.stream);
     check_kind(basis.kind);
     *n_entries = 0;
     const double D = wf->support_distance;
@@ -436,10 +458,22 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     double* dd = c.buf<double>(Context::kSlotDist, n_nodes);
     uint32_t* active = c.buf<uint32_t>(Context::kSlotActive, n_nodes);
     double* stage = c.buf<double>(Context::kSlotStage, 3 * n_nodes + 6 * nc);
-    IMB_CHECK(cudaMemcpyAsync(stage, nodes, n_nodes * 24, cudaMemcpyHostToDevice, c.stream));
-    aos_to_soa(c, stage, n_nodes, dx, dy, dz);
-    IMB_CHECK(cudaMemcpyAsync(dd, dist, n_nodes * 8, cudaMemcpyHostToDevice, c.stream));
     const bool exact = precision == IM_EXACT;
+    // nodes + distances through the pinned staging pool; the staging pass
+    // also checks for planar input (z == 0 everywhere -> the 2-D kernel)
+    std::atomic<bool> nonplanar{exact};
+    const H2DJob up[2] = {{stage, nodes, n_nodes * 24}, {dd, dist, n_nodes * 8}};
+    staged_h2d(c, up, 2, 192, [&](int job, const unsigned char* p, size_t, size_t len) {
+      if (job != 0 || nonplanar.load(std::memory_order_relaxed)) return;
+      const double* v = reinterpret_cast<const double*>(p);
+      for (size_t i = 2; i < len / 8; i += 3)
+        if (v[i] != 0.0) {
+          nonplanar.store(true, std::memory_order_relaxed);
+          return;
+        }
+    });
+    aos_to_soa(c, stage, n_nodes, dx, dy, dz);
+    tr.mark("h2d nodes+dist");
     double* tiles = c.buf<double>(Context::kSlotTiles, ctrl_tile_doubles(nc));
     double* boxes = nullptr;
     if (exact) {
@@ -453,10 +487,9 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
       boxes = c.buf<double>(Context::kSlotBoxes, 6 * (ctrl_padded(nc) / kCtrlTile));
       pack_controls_host(c, ctrl, alpha, nc, 1.0 / basis.support_radius, true, tiles, boxes);
     }
-    // planar input (z == 0 everywhere) runs the 2-D kernel
-    bool planar = true;
-    for (size_t i = 0; i < n_nodes && planar; ++i) planar = nodes[3 * i + 2] == 0.0;
+    bool planar = !nonplanar.load();
     for (size_t i = 0; i < nc && planar; ++i) planar = ctrl[3 * i + 2] == 0.0 && alpha[3 * i + 2] == 0.0;
+    tr.mark("controls + planar");
     EventTimer tm(c.stream);
     const size_t na = compact_active(c, dd, n_nodes, D, active);
     uint32_t* perm = nullptr;
@@ -483,14 +516,13 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     a.perm = perm;
     launch_volume(c, a);
     c.last_kernel_ms = tm.stop();
-    uint32_t* idx = reinterpret_cast<uint32_t*>(c.pinned.reserve(na * 4 + 16));
-    if (na) {
-      IMB_CHECK(cudaMemcpyAsync(idx, active, na * 4, cudaMemcpyDeviceToHost, c.stream));
-      IMB_CHECK(cudaMemcpyAsync(entry_values, vals, na * 24, cudaMemcpyDeviceToHost, c.stream));
-      IMB_CHECK(cudaStreamSynchronize(c.stream));
-    }
-    for (size_t i = 0; i < na; ++i) entry_nodes[i] = idx[i];
+    tr.mark("compact + order + kernel");
+    // ascending node ids (widened to size_t) + values, chunked through pinned
+    // memory (wall_distance.cpp:55-62 entry order)
+    const D2HJob down[2] = {{active, entry_nodes, na, 4, true}, {vals, entry_values, 3 * na, 8, false}};
+    staged_d2h(c, down, 2);
     *n_entries = na;
+    tr.mark("d2h");
   });
 }
 

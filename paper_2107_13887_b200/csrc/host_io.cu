@@ -1,0 +1,237 @@
+// host_io.cu — chunked, multi-threaded pinned staging for the C-ABI's host
+// arrays (see host_io.hpp).
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+
+#include <immintrin.h>
+
+#include "host_io.hpp"
+
+namespace imb {
+
+HostPool::HostPool(int threads) {
+  for (int i = 0; i < threads - 1; ++i) th_.emplace_back([this] { worker(); });
+}
+
+HostPool::~HostPool() {
+  {
+    std::lock_guard<std::mutex> g(m_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  for (auto& t : th_) t.join();
+}
+
+void HostPool::drain(const std::function<void(int)>& fn, int n) {
+  for (int i; (i = next_.fetch_add(1)) < n;) {
+    try {
+      fn(i);
+    } catch (...) {
+      std::lock_guard<std::mutex> g(m_);
+      if (!err_) err_ = std::current_exception();
+    }
+  }
+}
+
+void HostPool::worker() {
+  unsigned long long seen = 0;
+  for (;;) {
+    const std::function<void(int)>* fn;
+    int n;
+    {
+      std::unique_lock<std::mutex> l(m_);
+      cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      fn = fn_;
+      n = n_;
+    }
+    drain(*fn, n);
+    {
+      std::lock_guard<std::mutex> g(m_);
+      ++finished_;
+    }
+    done_.notify_all();
+  }
+}
+
+void HostPool::run(int n, const std::function<void(int)>& fn) {
+  if (n <= 0) return;
+  {
+    std::lock_guard<std::mutex> g(m_);
+    fn_ = &fn;
+    n_ = n;
+    next_.store(0);
+    err_ = nullptr;
+    finished_ = 0;
+    ++gen_;
+  }
+  cv_.notify_all();
+  drain(fn, n);
+  std::exception_ptr e;
+  {
+    // every worker acknowledges every generation, so none can still hold fn
+    std::unique_lock<std::mutex> l(m_);
+    done_.wait(l, [&] { return finished_ == (int)th_.size(); });
+    e = err_;
+    fn_ = nullptr;
+  }
+  if (e) std::rethrow_exception(e);
+}
+
+struct HostIOState {
+  HostPool pool;
+  HBuf<unsigned char> pin_in, pin_out;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t uploaded = nullptr;  // the last staged upload has left pin_in
+  explicit HostIOState(int threads) : pool(threads) {}
+  ~HostIOState() {
+    for (auto e : ev) cudaEventDestroy(e);
+    if (uploaded) cudaEventDestroy(uploaded);
+  }
+};
+
+namespace {
+
+constexpr size_t kChunk = 1u << 20;
+constexpr int kMaxEvents = 128;
+
+HostIOState& state(Context& c) {
+  if (!c.io) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    int threads = (int)std::max(1u, std::min(8u, hw ? hw : 1u));
+    if (const char* e = std::getenv("IMB_IO_THREADS")) threads = std::max(1, std::atoi(e));
+    c.io = std::make_shared<HostIOState>(threads);
+  }
+  return *c.io;
+}
+
+// memcpy into pinned staging with non-temporal (streaming) stores: the lines
+// go to DRAM instead of sitting dirty in the CPU caches, where the DMA engine
+// would have to snoop them out (measured: cached staging caps the H2D DMA at
+// ~15-19 GB/s on the B200 box, vs ~53 GB/s from DRAM).
+void copy_nt(unsigned char* dst, const unsigned char* src, size_t n) {
+  size_t i = 0;
+  while (i < n && (reinterpret_cast<uintptr_t>(dst + i) & 15)) dst[i] = src[i], ++i;
+  for (; i + 64 <= n; i += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+  }
+  for (; i < n; ++i) dst[i] = src[i];
+  _mm_sfence();
+}
+
+struct Chunk {
+  int job;
+  size_t off, len;  // bytes (h2d) or elements (d2h)
+  size_t stage;     // byte offset in the pinned buffer
+};
+
+}  // namespace
+
+void staged_h2d(Context& c, const H2DJob* jobs, int n_jobs, size_t align, const ChunkScan& scan) {
+  HostIOState& s = state(c);
+  size_t total = 0;
+  for (int j = 0; j < n_jobs; ++j) total += (jobs[j].bytes + 15) & ~size_t(15);
+  if (total == 0) return;
+  if (!s.uploaded) IMB_CHECK(cudaEventCreateWithFlags(&s.uploaded, cudaEventDisableTiming));
+  IMB_CHECK(cudaEventSynchronize(s.uploaded));  // pin_in is free again
+  unsigned char* pin = s.pin_in.reserve(total);
+  size_t chunk = kChunk;
+  if (const char* e = std::getenv("IMB_IO_CHUNK")) chunk = (size_t)std::atoll(e);
+  const size_t step = std::max(align, chunk / align * align);
+  std::vector<Chunk> chunks;
+  size_t stage = 0;
+  for (int j = 0; j < n_jobs; ++j) {
+    for (size_t off = 0; off < jobs[j].bytes; off += step)
+      chunks.push_back({j, off, std::min(step, jobs[j].bytes - off), stage + off});
+    stage += (jobs[j].bytes + 15) & ~size_t(15);
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  std::atomic<long long> memcpy_ns{0}, issue_ns{0};
+  static const bool nt = std::getenv("IMB_IO_NT") ? std::atoi(std::getenv("IMB_IO_NT")) != 0 : true;
+  s.pool.run((int)chunks.size(), [&](int i) {
+    const Chunk& k = chunks[i];
+    const H2DJob& jb = jobs[k.job];
+    unsigned char* dst = pin + k.stage;
+    const auto a = std::chrono::steady_clock::now();
+    if (nt)
+      copy_nt(dst, static_cast<const unsigned char*>(jb.src) + k.off, k.len);
+    else
+      std::memcpy(dst, static_cast<const unsigned char*>(jb.src) + k.off, k.len);
+    if (scan) scan(k.job, dst, k.off, k.len);
+    const auto b = std::chrono::steady_clock::now();
+    IMB_CHECK(cudaMemcpyAsync(static_cast<unsigned char*>(jb.dst) + k.off, dst, k.len,
+                              cudaMemcpyHostToDevice, c.stream));
+    const auto e = std::chrono::steady_clock::now();
+    memcpy_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(b - a).count();
+    issue_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(e - b).count();
+  });
+  IMB_CHECK(cudaEventRecord(s.uploaded, c.stream));
+  if (std::getenv("IMB_TRACE")) {
+    const auto t1 = std::chrono::steady_clock::now();
+    IMB_CHECK(cudaEventSynchronize(s.uploaded));
+    const auto t2 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[imb]   staged_h2d %zu B, %zu chunks, %d threads: run %.3f ms "
+                 "(memcpy %.3f, issue %.3f thread-ms), dma tail %.3f ms\n", total, chunks.size(),
+                 s.pool.size(), std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                 memcpy_ns * 1e-6, issue_ns * 1e-6,
+                 std::chrono::duration<double, std::milli>(t2 - t1).count());
+  }
+}
+
+void staged_d2h(Context& c, const D2HJob* jobs, int n_jobs) {
+  HostIOState& s = state(c);
+  size_t total = 0;
+  for (int j = 0; j < n_jobs; ++j) total += (jobs[j].count * jobs[j].src_size + 15) & ~size_t(15);
+  if (total == 0) return;
+  unsigned char* pin = s.pin_out.reserve(total);
+  const size_t target = std::max(kChunk, (total + kMaxEvents - 1) / kMaxEvents);
+  std::vector<Chunk> chunks;
+  size_t stage = 0;
+  for (int j = 0; j < n_jobs; ++j) {
+    const size_t per = std::max<size_t>(1, target / jobs[j].src_size);
+    for (size_t off = 0; off < jobs[j].count; off += per)
+      chunks.push_back({j, off, std::min(per, jobs[j].count - off),
+                        stage + off * jobs[j].src_size});
+    stage += (jobs[j].count * jobs[j].src_size + 15) & ~size_t(15);
+  }
+  while (s.ev.size() < chunks.size()) {
+    cudaEvent_t e;
+    IMB_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s.ev.push_back(e);
+  }
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    const Chunk& k = chunks[i];
+    const D2HJob& jb = jobs[k.job];
+    IMB_CHECK(cudaMemcpyAsync(pin + k.stage,
+                              static_cast<const unsigned char*>(jb.src) + k.off * jb.src_size,
+                              k.len * jb.src_size, cudaMemcpyDeviceToHost, c.stream));
+    IMB_CHECK(cudaEventRecord(s.ev[i], c.stream));
+  }
+  s.pool.run((int)chunks.size(), [&](int i) {
+    const Chunk& k = chunks[i];
+    const D2HJob& jb = jobs[k.job];
+    IMB_CHECK(cudaEventSynchronize(s.ev[i]));
+    if (jb.widen_u32) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(pin + k.stage);
+      uint64_t* dst = static_cast<uint64_t*>(jb.dst) + k.off;
+      for (size_t e = 0; e < k.len; ++e) dst[e] = src[e];
+    } else {
+      std::memcpy(static_cast<unsigned char*>(jb.dst) + k.off * jb.src_size, pin + k.stage,
+                  k.len * jb.src_size);
+    }
+  });
+}
+
+}  // namespace imb

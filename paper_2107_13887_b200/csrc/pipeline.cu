@@ -19,6 +19,7 @@
 
 #include "../../include/icemorph_b200.h"
 #include "greedy.hpp"
+#include "host_io.hpp"
 #include "runtime.hpp"
 
 namespace imb {
@@ -359,8 +360,8 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
     aos.reserve(3 * n_nodes);
     k_soa_to_aos<<<(n_nodes + 255) / 256, 256, 0, c.stream>>>(acc.x.p, acc.y.p, acc.z.p, n_nodes,
                                                                aos.p);
-    IMB_CHECK(cudaMemcpyAsync(deformed, aos.p, n_nodes * 24, cudaMemcpyDeviceToHost, c.stream));
-    IMB_CHECK(cudaStreamSynchronize(c.stream));
+    const D2HJob down{aos.p, deformed, 3 * n_nodes, 8, false};
+    staged_d2h(c, &down, 1);
     const double vol_s = since(t_vol);
 
     // surface accuracy (pipeline.cpp:87-99)

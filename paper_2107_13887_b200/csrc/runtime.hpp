@@ -12,6 +12,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdio>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -103,6 +104,8 @@ struct DPoints {
   }
 };
 
+struct HostIOState;  // host_io.cu: thread pool + pinned staging
+
 struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -121,6 +124,7 @@ struct Context {
     kSlotScanA, kSlotScanB, kSlotElemKind, kSlotElemOffset, kSlotElemNodes, kSlotCount
   };
   DBuf<unsigned char> slots[kSlotCount];
+  std::shared_ptr<HostIOState> io;  // created on first staged transfer
   template <class T>
   T* buf(Slot s, size_t count) {
     return reinterpret_cast<T*>(slots[s].reserve(count * sizeof(T) + 16));
