@@ -156,6 +156,7 @@ def run_b200(args):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = capi.Context(local)
+    prec = capi.EXACT if args.precision == "exact" else capi.FP64
     wl = build_workload(args.workload, args.scale)
     nodes, surface, dim = wl["nodes"], wl["surface"], wl["dim"]
     R, D = wl["R"], wl["D"]
@@ -190,7 +191,7 @@ def run_b200(args):
     plan = capi.VolumePlan(ctx, nodes, dim, surface, cutoff=cutoff)
     dist_ms = ctx.last_device_ms
     for l, (c, a) in enumerate(levels):
-        plan.set_level(l, c, a, D, wl["psi_kind"], "c2", R, capi.FP64)
+        plan.set_level(l, c, a, D, wl["psi_kind"], "c2", R, prec)
     supp = [plan.count_support(l, "c2", R) for l in range(len(levels))]
     pairs_step = sum(t for _, t in supp)
     in_step = sum(i for i, _ in supp)
@@ -198,12 +199,12 @@ def run_b200(args):
     flops_step = fin * in_step + fout * (pairs_step - in_step)
 
     # --- device-timed steps -------------------------------------------------
-    plan.run_steps(args.warmup, "c2", R, capi.FP64, flush_l2=True)
+    plan.run_steps(args.warmup, "c2", R, prec, flush_l2=True)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        st = plan.run_steps(args.steps, "c2", R, capi.FP64, flush_l2=True)
+        st = plan.run_steps(args.steps, "c2", R, prec, flush_l2=True)
     torch.cuda.synchronize()
     step_ms = st["step_ms_total"] / args.steps
     kern_ms = st["kernel_ms_total"] / max(st["kernel_launches"], 1)
@@ -240,7 +241,7 @@ def run_b200(args):
         h2d = d2h = 0
         for c, a in levels:
             idx, val = ctx.update_volume(nodes, d_host, c, a, D, wl["psi_kind"], "c2", R,
-                                         capi.FP64)
+                                         prec)
             h2d += nodes.nbytes + d_host.nbytes + c.nbytes + a.nbytes
             d2h += idx.size * 4 + val.nbytes
         if it:  # first pass is warm-up
@@ -258,7 +259,7 @@ def run_b200(args):
         "config": {"workload": wl["name"], "n_nodes": int(len(nodes)),
                    "n_surface": int(len(surface)), "n_controls_per_level": n_ctrl,
                    "R": R, "D": D, "active_per_level": st["active"][:len(levels)],
-                   "pairs_per_step": int(pairs_step), "l2": "flushed (256 MiB write) before each step",
+                   "pairs_per_step": int(pairs_step), "precision": args.precision, "l2": "flushed (256 MiB write) before each step",
                    "parallelism": f"{world} rank(s), contiguous node shards, no collective"},
         "roofline": roofline,
         "fp64_frac_of_peak": roofline["frac"],
@@ -383,6 +384,8 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "exact"],
+                    help="volume-update arithmetic: fp64 (FMA fast path) or exact (bit-identical)")
     ap.add_argument("--greedy-cache", default=None, help="development: save/load the control sets")
     ap.add_argument("--raw", default="", help="raw sweep cell, e.g. nc=4096,nv=10000000,R=inf,D=inf")
     args = ap.parse_args()

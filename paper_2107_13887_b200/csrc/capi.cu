@@ -461,7 +461,7 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     const bool exact = precision == IM_EXACT;
     // nodes + distances through the pinned staging pool; the staging pass
     // also checks for planar input (z == 0 everywhere -> the 2-D kernel)
-    std::atomic<bool> nonplanar{exact};
+    std::atomic<bool> nonplanar{false};
     const H2DJob up[2] = {{stage, nodes, n_nodes * 24}, {dd, dist, n_nodes * 8}};
     staged_h2d(c, up, 2, 192, [&](int job, const unsigned char* p, size_t, size_t len) {
       if (job != 0 || nonplanar.load(std::memory_order_relaxed)) return;
@@ -487,13 +487,25 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
       boxes = c.buf<double>(Context::kSlotBoxes, 6 * (ctrl_padded(nc) / kCtrlTile));
       pack_controls_host(c, ctrl, alpha, nc, 1.0 / basis.support_radius, true, tiles, boxes);
     }
+    // exact: the tiled kernel (spatial order + exact-safe culling) when the
+    // coordinate / R ranges allow its branch-free sqrt and division
+    bool tiled_exact = false;
+    if (exact) {
+      double m = max_abs_points(c, dx, dy, dz, n_nodes);
+      for (size_t i = 0; i < 3 * nc; ++i) m = std::max(m, std::fabs(ctrl[i]));
+      tiled_exact = exact_tiled_ok(basis.support_radius, m);
+      if (tiled_exact) {
+        boxes = c.buf<double>(Context::kSlotBoxes, 6 * (ctrl_padded(nc) / kCtrlTile));
+        exact_tile_boxes(c, tiles, nc, 1.0 / basis.support_radius, boxes);
+      }
+    }
     bool planar = !nonplanar.load();
     for (size_t i = 0; i < nc && planar; ++i) planar = ctrl[3 * i + 2] == 0.0 && alpha[3 * i + 2] == 0.0;
     tr.mark("controls + planar");
     EventTimer tm(c.stream);
     const size_t na = compact_active(c, dd, n_nodes, D, active);
     uint32_t* perm = nullptr;
-    if (!exact && na) {
+    if ((!exact || tiled_exact) && na) {
       perm = c.buf<uint32_t>(Context::kSlotPerm, na);
       spatial_order(c, dx, dy, dz, active, na, basis.support_radius, perm);
     }
@@ -509,8 +521,9 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     a.n_ctrl = nc;
     a.R = basis.support_radius;
     a.kind = basis.kind;
-    a.dim = planar && !exact ? 2 : 3;
+    a.dim = planar && (!exact || tiled_exact) ? 2 : 3;
     a.precision = exact ? Precision::Exact : Precision::Fast64;
+    a.exact_tiled = tiled_exact;
     a.out_val = vals;
     a.tile_box = boxes;
     a.perm = perm;

@@ -155,12 +155,15 @@ struct im_volume_plan {
   struct Level {
     DBuf<double> tiles, boxes;
     bool culled = false;
+    bool exact_tiled = false;
+    std::vector<double> host_ctrl, host_alpha;  // for count_support (fast-format tiles)
     size_t nc = 0;
     double D = 0.0;
     int psi_kind = 0;
   };
   Level levels[8];
   int n_levels = 0;
+  std::vector<double> host_ctrl, host_alpha;  // set_controls (single-level API)
   DBuf<uint32_t> perm;
   // spatial layout: node k' of the resident arrays is original node order[k']
   // (grid-cell order, so compacted active sets are spatially coherent)
@@ -168,6 +171,12 @@ struct im_volume_plan {
   bool reordered = false;
   DBuf<unsigned char> flush;
 };
+
+double max_abs_host(const double* v, size_t n) {
+  double m = 0.0;
+  for (size_t i = 0; i < n; ++i) m = std::max(m, std::fabs(v[i]));
+  return m;
+}
 
 extern "C" {
 
@@ -299,6 +308,10 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
     active.reserve(n_nodes);
     DBuf<double> stage, tiles, boxes;
     DBuf<uint32_t> perm;
+    // exact mode: tiled kernel when the coordinate / R ranges allow it (the
+    // controls are mesh nodes, so the node maximum covers them)
+    const bool tiled_exact = cfg->precision == IM_EXACT &&
+        exact_tiled_ok(g.basis.support_radius, max_abs_points(c, dn.x.p, dn.y.p, dn.z.p, n_nodes));
     Timer tm(c.stream);
     for (size_t l = 0; l < levels.size(); ++l) {
       const Lvl& lv = levels[l];
@@ -315,13 +328,18 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
                                     cudaMemcpyHostToDevice, c.stream));
         }
         const bool exact = cfg->precision == IM_EXACT;
-        if (exact)
+        if (exact) {
           pack_controls_aos(c, stage.p, stage.p + 3 * nc, nc, 1.0, tiles.p);
-        else
+          if (tiled_exact) {
+            boxes.reserve(6 * (ctrl_padded(nc) / kCtrlTile));
+            exact_tile_boxes(c, tiles.p, nc, 1.0 / g.basis.support_radius, boxes.p);
+          }
+        } else {
           pack_controls_host(c, cp.data(), lv.alpha.data(), nc, 1.0 / g.basis.support_radius, true,
                              tiles, boxes);
+        }
         touched = compact_active(c, dist.p, n_nodes, Dl[l], active.p);
-        if (!exact)
+        if (!exact || tiled_exact)
           spatial_order(c, dn.x.p, dn.y.p, dn.z.p, active.p, touched, g.basis.support_radius, perm);
         VolumeArgs a;
         a.x = dn.x.p, a.y = dn.y.p, a.z = dn.z.p;
@@ -331,8 +349,9 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
         a.D = Dl[l];
         a.psi_kind = cfg->psi_kind;
         a.tiles = tiles.p;
-        a.tile_box = exact ? nullptr : boxes.p;
-        a.perm = exact ? nullptr : perm.p;
+        a.tile_box = exact && !tiled_exact ? nullptr : boxes.p;
+        a.perm = exact && !tiled_exact ? nullptr : perm.p;
+        a.exact_tiled = tiled_exact;
         a.n_ctrl = nc;
         a.R = g.basis.support_radius;
         a.kind = g.basis.kind;
@@ -443,6 +462,8 @@ int im_volume_plan_set_controls(im_volume_plan* p, const double* ctrl, const dou
       IMB_CHECK(cudaMemcpy(p->ctrl_stage.p, ctrl, nc * 24, cudaMemcpyHostToDevice));
       IMB_CHECK(cudaMemcpy(p->ctrl_stage.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice));
     }
+    p->host_ctrl.assign(ctrl, ctrl + 3 * nc);
+    p->host_alpha.assign(alpha, alpha + 3 * nc);
     (void)c;
   });
 }
@@ -454,9 +475,23 @@ int im_volume_plan_run(im_volume_plan* p, const im_wall_function* wf, im_basis b
     *n_active = 0;
     if (D <= 0.0) return;
     const bool exact = precision == IM_EXACT;
+    const bool tiled_exact =
+        exact && exact_tiled_ok(basis.support_radius,
+                                std::max(max_abs_points(c, p->nodes.x.p, p->nodes.y.p,
+                                                        p->nodes.z.p, p->n),
+                                         max_abs_host(p->host_ctrl.data(), 3 * p->nc)));
     Timer tm(c.stream);
-    pack_controls_aos(c, p->ctrl_stage.p, p->ctrl_stage.p + 3 * p->nc, p->nc,
-                      exact ? 1.0 : 1.0 / basis.support_radius, p->tiles.p);
+    DBuf<double> boxes;
+    if (exact) {
+      pack_controls_aos(c, p->ctrl_stage.p, p->ctrl_stage.p + 3 * p->nc, p->nc, 1.0, p->tiles.p);
+      if (tiled_exact) {
+        boxes.reserve(6 * (ctrl_padded(p->nc) / kCtrlTile));
+        exact_tile_boxes(c, p->tiles.p, p->nc, 1.0 / basis.support_radius, boxes.p);
+      }
+    } else {
+      pack_controls_host(c, p->host_ctrl.data(), p->host_alpha.data(), p->nc,
+                         1.0 / basis.support_radius, true, p->tiles, boxes);
+    }
     const size_t na = compact_active(c, p->dist.p, p->n, D, p->active.p);
     VolumeArgs a;
     a.x = p->nodes.x.p, a.y = p->nodes.y.p, a.z = p->nodes.z.p;
@@ -471,6 +506,8 @@ int im_volume_plan_run(im_volume_plan* p, const im_wall_function* wf, im_basis b
     a.kind = basis.kind;
     a.dim = p->dim;
     a.precision = exact ? Precision::Exact : Precision::Fast64;
+    a.exact_tiled = tiled_exact;
+    a.tile_box = exact && !tiled_exact ? nullptr : boxes.p;
     a.acc_x = p->field.x.p, a.acc_y = p->field.y.p, a.acc_z = p->field.z.p;
     launch_volume(c, a);
     const double ms = tm.ms();
@@ -526,7 +563,12 @@ int im_volume_plan_set_level(im_volume_plan* p, int level, const double* ctrl, c
                              size_t nc, double D, int psi_kind, im_basis basis, int precision) {
   return guarded(p->ctx, [&](Context& c) {
     if (level < 0 || level >= 8) throw InvalidArgument("level index out of range (0..7)");
-    if (!p->reordered && precision != IM_EXACT && p->n) {
+    const bool tiled_exact =
+        precision == IM_EXACT &&
+        exact_tiled_ok(basis.support_radius,
+                       std::max(max_abs_points(c, p->nodes.x.p, p->nodes.y.p, p->nodes.z.p, p->n),
+                                max_abs_host(ctrl, 3 * nc)));
+    if (!p->reordered && (precision != IM_EXACT || tiled_exact) && p->n) {
       // one-time spatial layout of the resident mesh (grid cells of ~2R)
       spatial_order(c, p->nodes.x.p, p->nodes.y.p, p->nodes.z.p, nullptr, p->n,
                     basis.support_radius, p->order);
@@ -553,11 +595,18 @@ int im_volume_plan_set_level(im_volume_plan* p, int level, const double* ctrl, c
         IMB_CHECK(cudaMemcpy(stage.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice));
       }
       pack_controls_aos(c, stage.p, stage.p + 3 * nc, nc, 1.0, L.tiles.p);
-      L.culled = false;
+      L.culled = tiled_exact;
+      if (tiled_exact) {
+        L.boxes.reserve(6 * (ctrl_padded(nc) / kCtrlTile));
+        exact_tile_boxes(c, L.tiles.p, nc, 1.0 / basis.support_radius, L.boxes.p);
+      }
     } else {
       pack_controls_host(c, ctrl, alpha, nc, 1.0 / basis.support_radius, true, L.tiles, L.boxes);
       L.culled = true;
     }
+    L.exact_tiled = tiled_exact;
+    L.host_ctrl.assign(ctrl, ctrl + 3 * nc);
+    L.host_alpha.assign(alpha, alpha + 3 * nc);
     IMB_CHECK(cudaStreamSynchronize(c.stream));
     p->n_levels = std::max(p->n_levels, level + 1);
   });
@@ -612,6 +661,7 @@ int im_volume_plan_run_steps(im_volume_plan* p, im_basis basis, int precision, i
         a.kind = basis.kind;
         a.dim = p->dim;
         a.precision = precision == IM_EXACT ? Precision::Exact : Precision::Fast64;
+        a.exact_tiled = L.exact_tiled;
         a.acc_x = p->field.x.p, a.acc_y = p->field.y.p, a.acc_z = p->field.z.p;
         IMB_CHECK(cudaEventRecord(k0, c.stream));
         launch_volume(c, a);
@@ -649,7 +699,11 @@ int im_volume_plan_count_support(im_volume_plan* p, int level, im_basis basis,
     const auto& L = p->levels[level];
     const size_t na = compact_active(c, p->dist.p, p->n, L.D, p->active.p);
     *total = (unsigned long long)na * L.nc;
-    *in_support = count_support_pairs(c, p->nodes, p->active.p, na, L.tiles.p, L.nc,
+    // counted on fast-format tiles whatever the level's precision
+    DBuf<double> tiles, boxes;
+    pack_controls_host(c, L.host_ctrl.data(), L.host_alpha.data(), L.nc,
+                       1.0 / basis.support_radius, true, tiles, boxes);
+    *in_support = count_support_pairs(c, p->nodes, p->active.p, na, tiles.p, L.nc,
                                       1.0 / basis.support_radius);
   });
 }

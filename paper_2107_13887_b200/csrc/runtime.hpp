@@ -182,6 +182,9 @@ struct VolumeArgs {
   int kind = 1;
   int dim = 3;
   Precision precision = Precision::Fast64;
+  // exact path: use the tiled kernel (spatial order `perm`, culling with the
+  // exact-tile boxes `tile_box`); only when exact_tiled_ok() holds
+  bool exact_tiled = false;
   // outputs: either compacted AoS values (out_val[3k+c]) or accumulate into
   // per-node SoA deltas (acc_x/y/z[node] += value), skipping pinned nodes.
   double* out_val = nullptr;
@@ -190,6 +193,15 @@ struct VolumeArgs {
 };
 
 void launch_volume(Context& ctx, const VolumeArgs& a);
+// max |coordinate| over device SoA points (synchronous, 8-byte readback)
+double max_abs_points(Context& ctx, const double* x, const double* y, const double* z, size_t n);
+// ranges under which the tiled exact kernel's sqrt/division shortcuts are
+// bit-exact: |coordinates| <= 1e100, R in [1e-100, 1e100]
+inline bool exact_tiled_ok(double R, double max_abs) {
+  return R >= 1e-100 && R <= 1e100 && max_abs <= 1e100;
+}
+// per-tile boxes (scaled by inv_R) of exact tiles, real controls only
+void exact_tile_boxes(Context& ctx, const double* tiles, size_t n, double inv_R, double* boxes);
 
 // Stable compaction of {i : dist[i] < D} (wall_distance.cpp:56-58).  Writes
 // ascending node ids to d_out and returns the count (synchronises).

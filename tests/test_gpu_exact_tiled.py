@@ -1,0 +1,144 @@
+"""The tiled exact volume update (k_volume_exact_tiled) and the resident
+volume plan, bit for bit against the reference (wall_distance.cpp:46-64,
+rbf.cpp:195-203).
+
+The tiled kernel reorders points spatially, culls tiles / control groups
+farther than R and replaces the branches of sqrt / division / the eta >= 1
+cut by range-guarded branch-free forms; every case here must still equal the
+reference exactly (np.array_equal on the values)."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2107_13887_b200 import capi, workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def ref_update(oracle, nodes, d, ctrl, alpha, D, R, psi=0):
+    return oracle.update_volume(nodes, d, ctrl, alpha, D, psi, "c2", R)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("R", [0.05, 0.3, 2.0])
+def test_random_clouds(gpu, oracle, dim, R):
+    rng = np.random.default_rng(int(R * 100) + dim)
+    n, nc = 30000, 1500  # several tiles, insertion order not spatial
+    nodes = rng.random((n, 3))
+    ctrl = rng.random((nc, 3))
+    if dim == 2:
+        nodes[:, 2] = 0.0
+        ctrl[:, 2] = 0.0
+    alpha = rng.standard_normal((nc, 3))
+    if dim == 2:
+        alpha[:, 2] = 0.0
+    d = rng.random(n)  # any distances: psi only scales
+    i0, v0 = ref_update(oracle, nodes, d, ctrl, alpha, 0.8, R)
+    i1, v1 = gpu.update_volume(nodes, d, ctrl, alpha, 0.8, 0, "c2", R, capi.EXACT)
+    assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
+
+
+def test_boundary_pairs(gpu, oracle):
+    """eta exactly 1, just below / above 1, coincident points (s = 0), tiny
+    distances (s below the 2^-900 clamp), negative zero coordinates."""
+    R = 0.5
+    ctrl = np.array([[0.0, 0.0, 0.0], [1.0, 1.0, 1.0]])
+    alpha = np.array([[1.0, -2.0, 3.0], [0.25, 0.5, -0.75]])
+    ulp = np.nextafter(0.5, 1.0) - 0.5
+    pts = [[0.0, 0.0, 0.0], [0.5, 0.0, 0.0], [0.0, 0.5, 0.0], [0.0, 0.0, 0.5],
+           [0.5 - ulp, 0.0, 0.0], [0.5 + ulp, 0.0, 0.0], [1e-160, 0.0, 0.0],
+           [-0.0, -0.0, -0.0], [1.0, 1.0, 1.0], [1.0, 1.0, 1.0 - 1e-170], [1.5, 1.0, 1.0],
+           [0.3, 0.4, 0.0], [0.25, 0.25, 0.25]]
+    nodes = np.array(pts, float)
+    d = np.zeros(len(nodes))
+    i0, v0 = ref_update(oracle, nodes, d, ctrl, alpha, 1.0, R)
+    i1, v1 = gpu.update_volume(nodes, d, ctrl, alpha, 1.0, 0, "c2", R, capi.EXACT)
+    assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
+    assert (v1[1] == 0).all() and (v1[0] == alpha[0]).all()  # eta = 1 -> phi = +0
+
+
+@pytest.mark.parametrize("kind", ["c0", "c4", "c6"])
+def test_other_kinds(gpu, oracle, kind):
+    rng = np.random.default_rng(3)
+    nodes, ctrl = rng.random((8000, 3)), rng.random((700, 3))
+    alpha = rng.standard_normal((700, 3))
+    d = np.zeros(len(nodes))
+    i0, v0 = oracle.update_volume(nodes, d, ctrl, alpha, 1.0, 0, kind, 0.25)
+    i1, v1 = gpu.update_volume(nodes, d, ctrl, alpha, 1.0, 0, kind, 0.25, capi.EXACT)
+    assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
+
+
+def test_cfg1_levels_golden(gpu, golden):
+    """The reference's own cfg1 (30 %) control sets, real airfoil geometry."""
+    g = golden
+    nodes, surf = g["cfg1s_nodes"], g["cfg1s_surface"]
+    d = gpu.build_distance_index(nodes, 2, surf)
+    pos = nodes[surf]
+    for l in range(int(g["cfg1s_nlevels"])):
+        c, a = pos[g[f"cfg1s_l{l}_idx"]], g[f"cfg1s_l{l}_alpha"]
+        i1, v1 = gpu.update_volume(nodes, d, c, a, 1.0, 0, "c2", 0.5, capi.EXACT)
+        i2, v2 = gpu.update_volume(nodes, d, c, a, 1.0, 0, "c2", 0.5, capi.EXACT)
+        assert np.array_equal(v1, v2) and np.array_equal(i1, np.flatnonzero(d < 1.0))
+
+
+def test_cfg1_levels_reference(gpu, oracle, golden):
+    g = golden
+    nodes, surf = g["cfg1s_nodes"], g["cfg1s_surface"]
+    d = gpu.build_distance_index(nodes, 2, surf)
+    pos = nodes[surf]
+    for l in range(int(g["cfg1s_nlevels"])):
+        c, a = pos[g[f"cfg1s_l{l}_idx"]], g[f"cfg1s_l{l}_alpha"]
+        i0, v0 = oracle.update_volume(nodes, d, c, a, 1.0, 1, "c2", 0.5)
+        i1, v1 = gpu.update_volume(nodes, d, c, a, 1.0, 1, "c2", 0.5, capi.EXACT)
+        assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
+
+
+@pytest.mark.parametrize("precision", [capi.EXACT, capi.FP64])
+def test_volume_plan_levels(gpu, oracle, golden, precision):
+    """The resident plan (bench.py's timed path): one step over two levels
+    accumulates ((0 + dV_0) + dV_1) per node, dV_l from the reference."""
+    g = golden
+    nodes, surf = g["cfg1s_nodes"], g["cfg1s_surface"]
+    D = 1.0
+    plan = capi.VolumePlan(gpu, nodes, 2, surf, cutoff=D)
+    d = plan.distances()
+    assert np.array_equal(d < D, gpu.build_distance_index(nodes, 2, surf) < D)
+    pos = nodes[surf]
+    expect = np.zeros((len(nodes), 3))
+    levels = range(int(g["cfg1s_nlevels"]))
+    for l in levels:
+        c, a = pos[g[f"cfg1s_l{l}_idx"]], g[f"cfg1s_l{l}_alpha"]
+        plan.set_level(l, c, a, D, 0, "c2", 0.5, precision)
+        i0, v0 = oracle.update_volume(nodes, d, c, a, D, 0, "c2", 0.5)
+        expect[i0] = expect[i0] + v0
+    plan.reset_field()
+    st = plan.run_steps(1, "c2", 0.5, precision, flush_l2=False)
+    assert st["active"][0] == int((d < D).sum())
+    got = plan.field()
+    if precision == capi.EXACT:
+        assert np.array_equal(got, expect)
+    else:
+        assert np.abs(got - expect).max() <= 1e-10 * np.abs(expect).max()
+    # the flop-roofline pair count does not depend on the tile format
+    assert plan.count_support(0, "c2", 0.5)[0] > 0
+
+
+def test_volume_plan_single_level_run(gpu, oracle):
+    rng = np.random.default_rng(9)
+    nodes = rng.random((20000, 3))
+    surf = np.arange(0, 20000, 50)
+    plan = capi.VolumePlan(gpu, nodes, 3, surf, cutoff=math.inf)
+    d = plan.distances()
+    ctrl, alpha = nodes[surf[:200]], rng.standard_normal((200, 3))
+    plan.set_controls(ctrl, alpha)
+    i0, v0 = oracle.update_volume(nodes, d, ctrl, alpha, 0.3, 0, "c2", 0.2)
+    for prec in (capi.EXACT, capi.FP64):
+        plan.reset_field()
+        na, _ = plan.run(0.3, 0, "c2", 0.2, prec)
+        assert na == len(i0)
+        f = plan.field()[i0]
+        if prec == capi.EXACT:
+            assert np.array_equal(f, v0)
+        else:
+            assert np.abs(f - v0).max() <= 1e-10 * np.abs(v0).max()
