@@ -18,6 +18,13 @@ A step = the volume update of every level (stable compaction of d < D, then
 the update accumulated into the resident field) with the mesh resident in
 HBM; L2 is flushed (256 MiB write) before every timed step.
 
+Precision: the headline runs the EXACT mode (bit-identical to the reference:
+same per-pair IEEE operations and control order) because the reference's
+multilevel weights are so ill-conditioned on these configs (sum|alpha| /
+max|dV| up to 1e7-1e11) that any reordered / FMA-contracted evaluation
+differs from it by far more than the north star's 1e-10; the FP64 fast path
+is measured beside it (`fp64_fast`, with its measured deviation).
+
 `e2e` repeats the volume update through the public C-ABI call a user makes
 (im_update_volume, the reference's update_volume) with host buffers: H2D of
 nodes, distances and controls and D2H of the sparse update inside the timed
@@ -231,7 +238,9 @@ def run_b200(args):
                 "useful_flops_per_launch": useful_launch,
                 "flops_per_pair_in_support": fin,
                 "in_support_fraction": round(in_step / max(pairs_step, 1), 4),
-                "dense_equivalent_tflops": round(dense_tf, 3)}
+                "dense_equivalent_tflops": round(dense_tf, 3),
+                "fp64_instructions_per_pair": (30 if dim == 3 else 25) if prec == capi.EXACT
+                else (16 if dim == 3 else 14)}
 
     # --- e2e through the public C-ABI with host buffers ----------------------
     d_host = plan.distances()
@@ -270,12 +279,49 @@ def run_b200(args):
         "clocks": clk.summary(),
     }
     out.update(greedy)
+    if prec == capi.EXACT and not args.no_fast:
+        out["fp64_fast"] = fast_section(args, plan, levels, wl, R, D, pairs_step, fin, in_step,
+                                        launches_per_step, world, capi)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, levels, d_host, budget_s=args.cpu_seconds)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def fast_section(args, plan, levels, wl, R, D, pairs_step, fin, in_step, launches_per_step, world,
+                 capi):
+    """The FP64 fast path (FMA-contracted, Morton-ordered controls, rsqrt-based
+    distances) on the same resident plan: throughput, roofline fraction and
+    its measured deviation from the exact (reference-identical) field after
+    one step.  The deviation is bounded below by the conditioning of the
+    reference's weights (sum|alpha| / max|dV| reaches 1e7-1e11 on these
+    configs), which is why the headline uses the exact mode."""
+    plan.reset_field()
+    plan.run_steps(1, "c2", R, capi.EXACT, flush_l2=False)
+    f_exact = plan.field()
+    for l, (c, a) in enumerate(levels):
+        plan.set_level(l, c, a, D, wl["psi_kind"], "c2", R, capi.FP64)
+    plan.reset_field()
+    plan.run_steps(1, "c2", R, capi.FP64, flush_l2=False)
+    f_fast = plan.field()
+    plan.run_steps(args.warmup, "c2", R, capi.FP64, flush_l2=True)
+    st = plan.run_steps(args.steps, "c2", R, capi.FP64, flush_l2=True)
+    step_ms = st["step_ms_total"] / args.steps
+    kern_ms = st["kernel_ms_total"] / max(st["kernel_launches"], 1)
+    tf = fin * in_step / launches_per_step / (kern_ms * 1e-3) / 1e12
+    dev = float(np.abs(f_fast - f_exact).max())
+    scale = float(np.abs(f_exact).max())
+    disp = wl.get("disp")
+    smax = float(np.sqrt((disp ** 2).sum(axis=1)).max()) if disp is not None else None
+    return {"value": round(world * pairs_step / (step_ms * 1e-3) / 1e9, 3), "unit": UNIT,
+            "ms_per_step": round(step_ms, 4), "kernel_ms_avg": round(kern_ms, 4),
+            "roofline_frac": round(tf / FP64_PEAK_TFLOPS, 4), "achieved_tflops": round(tf, 3),
+            "max_abs_dev_vs_exact": dev,
+            "rel_dev_vs_max_field": dev / scale if scale else None,
+            "rel_dev_vs_max_surface_disp": dev / smax if smax else None,
+            "note": "FMA fast path; agreement limited by the reference weights' conditioning"}
 
 
 def cpu_baseline(wl, levels, dist, budget_s=12.0, nthreads=None):
@@ -384,8 +430,11 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--precision", default="fp64", choices=["fp64", "exact"],
-                    help="volume-update arithmetic: fp64 (FMA fast path) or exact (bit-identical)")
+    ap.add_argument("--precision", default="exact", choices=["fp64", "exact"],
+                    help="volume-update arithmetic of the headline: exact (bit-identical to the "
+                         "reference, default) or fp64 (FMA fast path)")
+    ap.add_argument("--no-fast", action="store_true",
+                    help="skip the secondary FP64 fast-path measurement")
     ap.add_argument("--greedy-cache", default=None, help="development: save/load the control sets")
     ap.add_argument("--raw", default="", help="raw sweep cell, e.g. nc=4096,nv=10000000,R=inf,D=inf")
     args = ap.parse_args()

@@ -121,7 +121,8 @@ struct Context {
   enum Slot : int {
     kSlotNodesX, kSlotNodesY, kSlotNodesZ, kSlotDist, kSlotActive, kSlotPerm, kSlotVals,
     kSlotTiles, kSlotBoxes, kSlotStage, kSlotCell, kSlotCounts, kSlotStart, kSlotBox,
-    kSlotScanA, kSlotScanB, kSlotElemKind, kSlotElemOffset, kSlotElemNodes, kSlotCount
+    kSlotScanA, kSlotScanB, kSlotElemKind, kSlotElemOffset, kSlotElemNodes, kSlotSortKeyA,
+    kSlotSortKeyB, kSlotSortTemp, kSlotCount
   };
   DBuf<unsigned char> slots[kSlotCount];
   std::shared_ptr<HostIOState> io;  // created on first staged transfer
