@@ -490,6 +490,7 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     // exact: the tiled kernel (spatial order + exact-safe culling) when the
     // coordinate / R ranges allow its branch-free sqrt and division
     bool tiled_exact = false;
+    double *midx = nullptr, *mbox = nullptr;
     if (exact) {
       double m = max_abs_points(c, dx, dy, dz, n_nodes);
       for (size_t i = 0; i < 3 * nc; ++i) m = std::max(m, std::fabs(ctrl[i]));
@@ -497,6 +498,9 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
       if (tiled_exact) {
         boxes = c.buf<double>(Context::kSlotBoxes, 6 * (ctrl_padded(nc) / kCtrlTile));
         exact_tile_boxes(c, tiles, nc, 1.0 / basis.support_radius, boxes);
+        midx = c.buf<double>(Context::kSlotIndex, 4 * ctrl_padded(nc));
+        mbox = c.buf<double>(Context::kSlotIndexBox, 6 * (ctrl_padded(nc) / kCtrlTile));
+        pack_exact_index_host(c, ctrl, nc, 1.0 / basis.support_radius, midx, mbox);
       }
     }
     bool planar = !nonplanar.load();
@@ -524,6 +528,8 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     a.dim = planar && (!exact || tiled_exact) ? 2 : 3;
     a.precision = exact ? Precision::Exact : Precision::Fast64;
     a.exact_tiled = tiled_exact;
+    a.ctrl_index = midx, a.index_box = mbox;
+    a.ctrl_diag = bbox_diagonal(ctrl, nc);
     a.out_val = vals;
     a.tile_box = boxes;
     a.perm = perm;

@@ -153,9 +153,10 @@ struct im_volume_plan {
   size_t nc = 0;
   // multi-level step (bench): per-level packed controls and support distance
   struct Level {
-    DBuf<double> tiles, boxes;
+    DBuf<double> tiles, boxes, midx, mbox;
     bool culled = false;
     bool exact_tiled = false;
+    double diag = 0.0;
     std::vector<double> host_ctrl, host_alpha;  // for count_support (fast-format tiles)
     size_t nc = 0;
     double D = 0.0;
@@ -306,7 +307,7 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
     const bool planar = dim == 2 && all_z_zero(nodes, n_nodes);
     DBuf<uint32_t> active;
     active.reserve(n_nodes);
-    DBuf<double> stage, tiles, boxes;
+    DBuf<double> stage, tiles, boxes, midx, mbox;
     DBuf<uint32_t> perm;
     // exact mode: tiled kernel when the coordinate / R ranges allow it (the
     // controls are mesh nodes, so the node maximum covers them)
@@ -333,6 +334,9 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
           if (tiled_exact) {
             boxes.reserve(6 * (ctrl_padded(nc) / kCtrlTile));
             exact_tile_boxes(c, tiles.p, nc, 1.0 / g.basis.support_radius, boxes.p);
+            midx.reserve(4 * ctrl_padded(nc));
+            mbox.reserve(6 * (ctrl_padded(nc) / kCtrlTile));
+            pack_exact_index_host(c, cp.data(), nc, 1.0 / g.basis.support_radius, midx.p, mbox.p);
           }
         } else {
           pack_controls_host(c, cp.data(), lv.alpha.data(), nc, 1.0 / g.basis.support_radius, true,
@@ -352,6 +356,9 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
         a.tile_box = exact && !tiled_exact ? nullptr : boxes.p;
         a.perm = exact && !tiled_exact ? nullptr : perm.p;
         a.exact_tiled = tiled_exact;
+        a.ctrl_index = tiled_exact ? midx.p : nullptr;
+        a.index_box = tiled_exact ? mbox.p : nullptr;
+        a.ctrl_diag = bbox_diagonal(cp.data(), nc);
         a.n_ctrl = nc;
         a.R = g.basis.support_radius;
         a.kind = g.basis.kind;
@@ -481,12 +488,16 @@ int im_volume_plan_run(im_volume_plan* p, const im_wall_function* wf, im_basis b
                                                         p->nodes.z.p, p->n),
                                          max_abs_host(p->host_ctrl.data(), 3 * p->nc)));
     Timer tm(c.stream);
-    DBuf<double> boxes;
+    DBuf<double> boxes, midx, mbox;
     if (exact) {
       pack_controls_aos(c, p->ctrl_stage.p, p->ctrl_stage.p + 3 * p->nc, p->nc, 1.0, p->tiles.p);
       if (tiled_exact) {
         boxes.reserve(6 * (ctrl_padded(p->nc) / kCtrlTile));
         exact_tile_boxes(c, p->tiles.p, p->nc, 1.0 / basis.support_radius, boxes.p);
+        midx.reserve(4 * ctrl_padded(p->nc));
+        mbox.reserve(6 * (ctrl_padded(p->nc) / kCtrlTile));
+        pack_exact_index_host(c, p->host_ctrl.data(), p->nc, 1.0 / basis.support_radius, midx.p,
+                              mbox.p);
       }
     } else {
       pack_controls_host(c, p->host_ctrl.data(), p->host_alpha.data(), p->nc,
@@ -507,6 +518,9 @@ int im_volume_plan_run(im_volume_plan* p, const im_wall_function* wf, im_basis b
     a.dim = p->dim;
     a.precision = exact ? Precision::Exact : Precision::Fast64;
     a.exact_tiled = tiled_exact;
+    a.ctrl_index = tiled_exact ? midx.p : nullptr;
+    a.index_box = tiled_exact ? mbox.p : nullptr;
+    a.ctrl_diag = bbox_diagonal(p->host_ctrl.data(), p->nc);
     a.tile_box = exact && !tiled_exact ? nullptr : boxes.p;
     a.acc_x = p->field.x.p, a.acc_y = p->field.y.p, a.acc_z = p->field.z.p;
     launch_volume(c, a);
@@ -599,12 +613,16 @@ int im_volume_plan_set_level(im_volume_plan* p, int level, const double* ctrl, c
       if (tiled_exact) {
         L.boxes.reserve(6 * (ctrl_padded(nc) / kCtrlTile));
         exact_tile_boxes(c, L.tiles.p, nc, 1.0 / basis.support_radius, L.boxes.p);
+        L.midx.reserve(4 * ctrl_padded(nc));
+        L.mbox.reserve(6 * (ctrl_padded(nc) / kCtrlTile));
+        pack_exact_index_host(c, ctrl, nc, 1.0 / basis.support_radius, L.midx.p, L.mbox.p);
       }
     } else {
       pack_controls_host(c, ctrl, alpha, nc, 1.0 / basis.support_radius, true, L.tiles, L.boxes);
       L.culled = true;
     }
     L.exact_tiled = tiled_exact;
+    L.diag = bbox_diagonal(ctrl, nc);
     L.host_ctrl.assign(ctrl, ctrl + 3 * nc);
     L.host_alpha.assign(alpha, alpha + 3 * nc);
     IMB_CHECK(cudaStreamSynchronize(c.stream));
@@ -662,6 +680,9 @@ int im_volume_plan_run_steps(im_volume_plan* p, im_basis basis, int precision, i
         a.dim = p->dim;
         a.precision = precision == IM_EXACT ? Precision::Exact : Precision::Fast64;
         a.exact_tiled = L.exact_tiled;
+        a.ctrl_index = L.exact_tiled ? L.midx.p : nullptr;
+        a.index_box = L.exact_tiled ? L.mbox.p : nullptr;
+        a.ctrl_diag = L.diag;
         a.acc_x = p->field.x.p, a.acc_y = p->field.y.p, a.acc_z = p->field.z.p;
         IMB_CHECK(cudaEventRecord(k0, c.stream));
         launch_volume(c, a);

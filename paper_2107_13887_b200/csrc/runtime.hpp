@@ -122,7 +122,7 @@ struct Context {
     kSlotNodesX, kSlotNodesY, kSlotNodesZ, kSlotDist, kSlotActive, kSlotPerm, kSlotVals,
     kSlotTiles, kSlotBoxes, kSlotStage, kSlotCell, kSlotCounts, kSlotStart, kSlotBox,
     kSlotScanA, kSlotScanB, kSlotElemKind, kSlotElemOffset, kSlotElemNodes, kSlotSortKeyA,
-    kSlotSortKeyB, kSlotSortTemp, kSlotCount
+    kSlotSortKeyB, kSlotSortTemp, kSlotIndex, kSlotIndexBox, kSlotBlockOrder, kSlotCount
   };
   DBuf<unsigned char> slots[kSlotCount];
   std::shared_ptr<HostIOState> io;  // created on first staged transfer
@@ -186,6 +186,14 @@ struct VolumeArgs {
   // exact path: use the tiled kernel (spatial order `perm`, culling with the
   // exact-tile boxes `tile_box`); only when exact_tiled_ok() holds
   bool exact_tiled = false;
+  // exact tiled: Morton index of the controls (pack_exact_index_host) for the
+  // gathered kernel; null = group culling over the insertion order only
+  const double* ctrl_index = nullptr;
+  const double* index_box = nullptr;
+  double ctrl_diag = 0.0;  // diagonal of the controls' bounding box (gather heuristic)
+  // exact tiled kernel: CTA i processes block cta_order[i] of kExactBlock
+  // positions (heaviest first, block_order()); null = natural order
+  const uint32_t* cta_order = nullptr;
   // outputs: either compacted AoS values (out_val[3k+c]) or accumulate into
   // per-node SoA deltas (acc_x/y/z[node] += value), skipping pinned nodes.
   double* out_val = nullptr;
@@ -201,6 +209,21 @@ double max_abs_points(Context& ctx, const double* x, const double* y, const doub
 inline bool exact_tiled_ok(double R, double max_abs) {
   return R >= 1e-100 && R <= 1e100 && max_abs <= 1e100;
 }
+// Morton index of the controls for the gathered exact kernel: tiles of 256
+// (cx, cy, cz, insertion index) raw + per-tile boxes scaled by inv_R
+// (device buffers of 4*ctrl_padded(n) and 6*ctrl_padded(n)/256 doubles)
+void pack_exact_index_host(Context& ctx, const double* ctrl, size_t n, double inv_R, double* d_midx,
+                           double* d_mbox);
+// positions per CTA of the exact tiled kernel (128 threads x 2 points)
+constexpr int kExactBlock = 256;
+// longest-first processing order of the exact kernel's blocks: per block of
+// bp ordered positions, the count of controls within R of its box, sorted
+// descending (writes ceil(n / bp) block ids to `order`)
+void block_order(Context& ctx, const double* x, const double* y, const double* z,
+                 const uint32_t* active, const uint32_t* perm, size_t n, int bp,
+                 const double* exact_tiles, size_t nc, double R, uint32_t* order);
+// diagonal of the bounding box of n AoS points (host)
+double bbox_diagonal(const double* xyz, size_t n);
 // per-tile boxes (scaled by inv_R) of exact tiles, real controls only
 void exact_tile_boxes(Context& ctx, const double* tiles, size_t n, double inv_R, double* boxes);
 

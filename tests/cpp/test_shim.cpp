@@ -103,6 +103,25 @@ int main() {
   for (std::size_t k : outer.nodes) CHECK(deformed.nodes[k] == ring.nodes[k]);
   CHECK(report.surface_max_error < 1e-3);
   CHECK(!report.levels.empty() && report.total_control_points() > 0);
+  CHECK(report.inverted_elements == 0);  // ring has no elements
+
+  // quality.cpp:100-148 (test_quality.cpp:68-78, 115-128)
+  Mesh tri;
+  tri.dim = 2;
+  tri.nodes = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}};
+  tri.elements = {{ElementKind::Triangle, {0, 1, 2}}, {ElementKind::Triangle, {0, 2, 1}}};
+  CHECK(signed_measure(tri, tri.elements[0]) == 0.5);
+  CHECK(signed_measures(tri)[1] == -0.5);
+  CHECK(count_inverted(tri) == 1);
+  Mesh cube;
+  cube.dim = 3;
+  for (int k = 0; k < 2; ++k)
+    for (int j = 0; j < 2; ++j)
+      for (int i = 0; i < 2; ++i) cube.nodes.push_back({double(i), double(j), double(k)});
+  cube.elements = {{ElementKind::Hexahedron, {0, 1, 3, 2, 4, 5, 7, 6}}};
+  CHECK(std::abs(signed_measure(cube, cube.elements[0]) - 1.0) < 1e-14);
+  cube.elements[0].nodes = {4, 5, 7, 6, 0, 1, 3, 2};
+  CHECK(count_inverted(cube) == 1);
   std::printf(failures ? "shim: %d FAILED\n" : "shim: all passed\n", failures);
   return failures ? 1 : 0;
 }

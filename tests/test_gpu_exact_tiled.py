@@ -20,9 +20,18 @@ def ref_update(oracle, nodes, d, ctrl, alpha, D, R, psi=0):
     return oracle.update_volume(nodes, d, ctrl, alpha, D, psi, "c2", R)
 
 
+@pytest.fixture(params=["auto", "no_gather"])
+def launch_shape(request, monkeypatch):
+    """Both exact kernels: gathered (R < 15 % of the control spread) and
+    group-culled (IMB_NO_GATHER)."""
+    if request.param == "no_gather":
+        monkeypatch.setenv("IMB_NO_GATHER", "1")
+    return request.param
+
+
 @pytest.mark.parametrize("dim", [2, 3])
 @pytest.mark.parametrize("R", [0.05, 0.3, 2.0])
-def test_random_clouds(gpu, oracle, dim, R):
+def test_random_clouds(gpu, oracle, dim, R, launch_shape):
     rng = np.random.default_rng(int(R * 100) + dim)
     n, nc = 30000, 1500  # several tiles, insertion order not spatial
     nodes = rng.random((n, 3))
@@ -39,7 +48,7 @@ def test_random_clouds(gpu, oracle, dim, R):
     assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
 
 
-def test_boundary_pairs(gpu, oracle):
+def test_boundary_pairs(gpu, oracle, launch_shape):
     """eta exactly 1, just below / above 1, coincident points (s = 0), tiny
     distances (s below the 2^-900 clamp), negative zero coordinates."""
     R = 0.5
@@ -82,7 +91,7 @@ def test_cfg1_levels_golden(gpu, golden):
         assert np.array_equal(v1, v2) and np.array_equal(i1, np.flatnonzero(d < 1.0))
 
 
-def test_cfg1_levels_reference(gpu, oracle, golden):
+def test_cfg1_levels_reference(gpu, oracle, golden, launch_shape):
     g = golden
     nodes, surf = g["cfg1s_nodes"], g["cfg1s_surface"]
     d = gpu.build_distance_index(nodes, 2, surf)
@@ -95,7 +104,7 @@ def test_cfg1_levels_reference(gpu, oracle, golden):
 
 
 @pytest.mark.parametrize("precision", [capi.EXACT, capi.FP64])
-def test_volume_plan_levels(gpu, oracle, golden, precision):
+def test_volume_plan_levels(gpu, oracle, golden, precision, launch_shape):
     """The resident plan (bench.py's timed path): one step over two levels
     accumulates ((0 + dV_0) + dV_1) per node, dV_l from the reference."""
     g = golden
