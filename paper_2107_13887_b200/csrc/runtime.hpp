@@ -221,7 +221,7 @@ constexpr int kExactBlock = 256;
 // descending (writes ceil(n / bp) block ids to `order`)
 void block_order(Context& ctx, const double* x, const double* y, const double* z,
                  const uint32_t* active, const uint32_t* perm, size_t n, int bp,
-                 const double* exact_tiles, size_t nc, double R, uint32_t* order);
+                 const double* tiles, size_t nc, double R, bool fast_tiles, uint32_t* order);
 // diagonal of the bounding box of n AoS points (host)
 double bbox_diagonal(const double* xyz, size_t n);
 // per-tile boxes (scaled by inv_R) of exact tiles, real controls only
