@@ -157,6 +157,8 @@ struct im_volume_plan {
     bool culled = false;
     bool exact_tiled = false;
     double diag = 0.0;
+    DBuf<uint32_t> order;  // cached longest-first block order (exact kernel)
+    size_t order_n = 0;
     std::vector<double> host_ctrl, host_alpha;  // for count_support (fast-format tiles)
     size_t nc = 0;
     double D = 0.0;
@@ -623,6 +625,7 @@ int im_volume_plan_set_level(im_volume_plan* p, int level, const double* ctrl, c
     }
     L.exact_tiled = tiled_exact;
     L.diag = bbox_diagonal(ctrl, nc);
+    L.order_n = 0;  // block order recomputed at the next run
     L.host_ctrl.assign(ctrl, ctrl + 3 * nc);
     L.host_alpha.assign(alpha, alpha + 3 * nc);
     IMB_CHECK(cudaStreamSynchronize(c.stream));
@@ -655,7 +658,7 @@ int im_volume_plan_run_steps(im_volume_plan* p, im_basis basis, int precision, i
       double last_D = NAN;
       size_t last_na = 0;
       for (int l = 0; l < p->n_levels; ++l) {
-        const auto& L = p->levels[l];
+        auto& L = p->levels[l];
         if (L.D <= 0.0) continue;
         // compaction + spatial order, shared by consecutive levels with the same D
         size_t na = last_na;
@@ -683,6 +686,16 @@ int im_volume_plan_run_steps(im_volume_plan* p, im_basis basis, int precision, i
         a.ctrl_index = L.exact_tiled ? L.midx.p : nullptr;
         a.index_box = L.exact_tiled ? L.mbox.p : nullptr;
         a.ctrl_diag = L.diag;
+        if (exact_uses_block_order(a)) {
+          // the active set of a level is the same every step (stable compaction)
+          if (L.order_n != na) {
+            L.order.reserve(na / kExactBlock + 1);
+            block_order(c, a.x, a.y, a.z, a.active, nullptr, na, kExactBlock, L.tiles.p, L.nc,
+                        basis.support_radius, false, L.order.p);
+            L.order_n = na;
+          }
+          a.cta_order = L.order.p;
+        }
         a.acc_x = p->field.x.p, a.acc_y = p->field.y.p, a.acc_z = p->field.z.p;
         IMB_CHECK(cudaEventRecord(k0, c.stream));
         launch_volume(c, a);

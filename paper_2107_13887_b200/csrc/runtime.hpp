@@ -222,6 +222,9 @@ constexpr int kExactBlock = 256;
 void block_order(Context& ctx, const double* x, const double* y, const double* z,
                  const uint32_t* active, const uint32_t* perm, size_t n, int bp,
                  const double* tiles, size_t nc, double R, bool fast_tiles, uint32_t* order);
+// whether launch_volume(a) runs the exact tiled kernel with a block order
+// (callers may cache block_order() results and pass them as a.cta_order)
+bool exact_uses_block_order(const VolumeArgs& a);
 // diagonal of the bounding box of n AoS points (host)
 double bbox_diagonal(const double* xyz, size_t n);
 // per-tile boxes (scaled by inv_R) of exact tiles, real controls only
