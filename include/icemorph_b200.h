@@ -161,6 +161,22 @@ int im_count_inverted(im_context* ctx, const double* nodes, size_t n_nodes,
                       const int* element_kinds, const size_t* element_offsets,
                       const size_t* element_nodes, size_t n_elements, size_t* inverted);
 
+/* orthogonality, quality.hpp (quality.cpp:150-236): per-element scores in
+ * degrees (nullable, n_elements doubles) and signed measures (nullable), the
+ * report scalars in *report.  Faces are matched on the device (sorted node
+ * keys, radix sort) instead of the reference's std::map; scores agree with
+ * the reference to ~1e-13 degrees (CUDA atan2), measures and counts exactly. */
+typedef struct {
+  double min_orthogonality_deg;
+  double mean_orthogonality_deg;
+  size_t inverted_count;
+  size_t degenerate_count;
+} im_quality_report;
+int im_orthogonality(im_context* ctx, const double* nodes, size_t n_nodes,
+                     const int* element_kinds, const size_t* element_offsets,
+                     const size_t* element_nodes, size_t n_elements, double* element_scores,
+                     double* element_measures, im_quality_report* report);
+
 /* ---- pipeline -----------------------------------------------------------------
  * deform, pipeline.hpp:54-56 (pipeline.cpp:19-106) on a mesh given as its
  * node array and the node lists of the deforming patch and of the pinned
@@ -172,8 +188,8 @@ int im_count_inverted(im_context* ctx, const double* nodes, size_t n_nodes,
  * slots.  When the config carries the mesh's volume elements (CSR as for
  * im_signed_measures; n_elements = 0 for none) the report's
  * inverted_elements is count_inverted(deformed) (pipeline.cpp:101),
- * evaluated on the device-resident deformed nodes; the orthogonality
- * quality report (compute_quality) is out of scope. */
+ * evaluated on the device-resident deformed nodes; with compute_quality the
+ * orthogonality reports of the mesh before and after (has_quality = 1). */
 typedef struct {
   im_greedy_config greedy;
   double volume_k;
@@ -184,6 +200,7 @@ typedef struct {
   const size_t* element_offsets;
   const size_t* element_nodes;
   size_t n_elements;
+  int compute_quality; /* with elements: quality_before / quality_after (pipeline.cpp:55, 102) */
 } im_deform_config;
 
 typedef struct {
@@ -196,6 +213,9 @@ typedef struct {
   double distance_seconds;
   double volume_seconds;
   size_t inverted_elements;
+  int has_quality;
+  im_quality_report quality_before;
+  im_quality_report quality_after;
 } im_deform_report;
 
 int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,

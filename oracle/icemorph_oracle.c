@@ -552,3 +552,185 @@ int or_signed_measures(const double* nodes, size_t n_nodes, int dim, const int* 
   *inverted = count;
   return 0;
 }
+
+/* ---- quality.cpp:150-236 (orthogonality) ------------------------------------ */
+/* element_faces, quality.cpp:19-49: local node lists per kind */
+static const int kFaceCount[7] = {0, 3, 4, 4, 6, 5, 5};
+static const int kFaceNodes[7][6][5] = {
+    /* count, nodes... */
+    {{0}},
+    {{2, 0, 1}, {2, 1, 2}, {2, 2, 0}},
+    {{2, 0, 1}, {2, 1, 2}, {2, 2, 3}, {2, 3, 0}},
+    {{3, 0, 1, 2}, {3, 0, 1, 3}, {3, 1, 2, 3}, {3, 0, 2, 3}},
+    {{4, 0, 1, 2, 3}, {4, 4, 5, 6, 7}, {4, 0, 1, 5, 4}, {4, 1, 2, 6, 5}, {4, 2, 3, 7, 6},
+     {4, 3, 0, 4, 7}},
+    {{3, 0, 1, 2}, {3, 3, 4, 5}, {4, 0, 1, 4, 3}, {4, 1, 2, 5, 4}, {4, 2, 0, 3, 5}},
+    {{4, 0, 1, 2, 3}, {3, 0, 1, 4}, {3, 1, 2, 4}, {3, 2, 3, 4}, {3, 3, 0, 4}},
+};
+
+typedef struct {
+  size_t key[4]; /* sorted global nodes, padded with SIZE_MAX */
+  size_t seq;    /* insertion order (element-major, face order) */
+  size_t elem;
+  int face;
+} FaceRec;
+
+static int face_cmp(const void* a, const void* b) {
+  const FaceRec* x = (const FaceRec*)a;
+  const FaceRec* y = (const FaceRec*)b;
+  for (int k = 0; k < 4; ++k)
+    if (x->key[k] != y->key[k]) return x->key[k] < y->key[k] ? -1 : 1;
+  return x->seq < y->seq ? -1 : (x->seq > y->seq ? 1 : 0);
+}
+
+typedef struct { double x, y, z; } V3;
+static V3 v3(double x, double y, double z) { V3 r = {x, y, z}; return r; }
+static V3 vsub(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }
+static V3 vadd(V3 a, V3 b) { return v3(a.x + b.x, a.y + b.y, a.z + b.z); }
+static V3 vscale(V3 a, double s) { return v3(a.x * s, a.y * s, a.z * s); }
+static double vsq(V3 a) { return a.x * a.x + a.y * a.y + a.z * a.z; }
+static double vdot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+static V3 vcross(V3 a, V3 b) {
+  return v3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+/* vec.hpp:64-67 */
+static V3 vnormalized(V3 v) {
+  const double n = sqrt(vsq(v));
+  return n > 0.0 ? vscale(v, 1.0 / n) : v3(0, 0, 0);
+}
+static V3 node_at(const double* nodes, size_t i) { return v3(nodes[3 * i], nodes[3 * i + 1], nodes[3 * i + 2]); }
+
+/* quality.cpp:51-55 / 74-78: sum in node order, times 1/count */
+static V3 centroid_of(const double* nodes, const size_t* g, size_t cnt) {
+  V3 c = v3(0, 0, 0);
+  for (size_t k = 0; k < cnt; ++k) c = vadd(c, node_at(nodes, g[k]));
+  return vscale(c, 1.0 / (double)cnt);
+}
+
+/* quality.cpp:57-72 */
+static V3 face_normal(const double* nodes, const size_t* g, int count) {
+  if (count == 2) {
+    const V3 t = vsub(node_at(nodes, g[1]), node_at(nodes, g[0]));
+    return vnormalized(v3(t.y, -t.x, 0.0));
+  }
+  const V3 a = node_at(nodes, g[0]), b = node_at(nodes, g[1]), c = node_at(nodes, g[2]);
+  V3 n = vcross(vsub(b, a), vsub(c, a));
+  if (count == 4) {
+    const V3 d = node_at(nodes, g[3]);
+    n = vadd(vnormalized(n), vnormalized(vcross(vsub(c, a), vsub(d, a))));
+  }
+  return vnormalized(n);
+}
+
+/* quality.cpp:82-88 */
+static double face_score(V3 normal, V3 line) {
+  const V3 c = vnormalized(line);
+  if (vsq(normal) == 0.0 || vsq(c) == 0.0) return 0.0;
+  const double along = fabs(vdot(normal, c));
+  const double transverse = sqrt(vsq(vcross(normal, c)));
+  return 90.0 - atan2(transverse, along) * 180.0 / 3.141592653589793;
+}
+
+static void face_global(const size_t* conn, const size_t* offsets, const int* kinds, size_t e,
+                        int f, size_t* g, int* count) {
+  const int* fn = kFaceNodes[kinds[e]][f];
+  *count = fn[0];
+  for (int k = 0; k < fn[0]; ++k) g[k] = conn[offsets[e] + fn[1 + k]];
+}
+
+int or_orthogonality(const double* nodes, size_t n_nodes, int dim, const int* kinds,
+                     const size_t* offsets, const size_t* conn, size_t n_elem, double* out_scores,
+                     double* out_measures, double* out_min, double* out_mean,
+                     size_t* out_inverted, size_t* out_degenerate) {
+  size_t inverted = 0;
+  or_signed_measures(nodes, n_nodes, dim, kinds, offsets, conn, n_elem, out_measures, &inverted);
+  *out_inverted = inverted;
+  *out_degenerate = 0;
+  *out_min = 90.0;
+  *out_mean = 90.0;
+  for (size_t e = 0; e < n_elem; ++e) out_scores[e] = 90.0;
+  if (n_elem == 0) return 0;
+  size_t nf = 0;
+  for (size_t e = 0; e < n_elem; ++e) nf += (size_t)kFaceCount[kinds[e]];
+  FaceRec* recs = (FaceRec*)malloc((nf ? nf : 1) * sizeof(FaceRec));
+  V3* cen = (V3*)malloc(n_elem * sizeof(V3));
+  double* internal = (double*)malloc(n_elem * sizeof(double));
+  double* boundary = (double*)malloc(n_elem * sizeof(double));
+  char* degen = (char*)calloc(n_elem, 1);
+  size_t r = 0;
+  for (size_t e = 0; e < n_elem; ++e) {
+    for (int f = 0; f < kFaceCount[kinds[e]]; ++f) {
+      size_t g[4];
+      int cnt;
+      face_global(conn, offsets, kinds, e, f, g, &cnt);
+      FaceRec* fr = &recs[r];
+      for (int k = 0; k < 4; ++k) fr->key[k] = k < cnt ? g[k] : (size_t)-1;
+      for (int a = 1; a < cnt; ++a) /* insertion sort of the key */
+        for (int b = a; b > 0 && fr->key[b - 1] > fr->key[b]; --b) {
+          const size_t t = fr->key[b];
+          fr->key[b] = fr->key[b - 1];
+          fr->key[b - 1] = t;
+        }
+      fr->seq = r;
+      fr->elem = e;
+      fr->face = f;
+      ++r;
+    }
+    cen[e] = centroid_of(nodes, conn + offsets[e], offsets[e + 1] - offsets[e]);
+    internal[e] = -1.0;
+    boundary[e] = -1.0;
+  }
+  qsort(recs, nf, sizeof(FaceRec), face_cmp);
+  for (size_t i = 0; i < nf;) {
+    size_t j = i + 1;
+    while (j < nf && memcmp(recs[j].key, recs[i].key, sizeof recs[i].key) == 0) ++j;
+    size_t g0[4];
+    int cnt;
+    face_global(conn, offsets, kinds, recs[i].elem, recs[i].face, g0, &cnt);
+    const V3 normal = face_normal(nodes, g0, cnt);
+    const int is_deg = vsq(normal) == 0.0;
+    if (j - i == 2) {
+      const V3 line = vsub(cen[recs[i + 1].elem], cen[recs[i].elem]);
+      const double score = is_deg ? 0.0 : face_score(normal, line);
+      for (size_t u = i; u < j; ++u) {
+        double* slot = &internal[recs[u].elem];
+        *slot = *slot < 0.0 ? score : (*slot < score ? *slot : score); /* fold_in */
+        if (is_deg) degen[recs[u].elem] = 1;
+      }
+    } else {
+      for (size_t u = i; u < j; ++u) {
+        size_t gu[4];
+        int cu;
+        face_global(conn, offsets, kinds, recs[u].elem, recs[u].face, gu, &cu);
+        const V3 line = vsub(centroid_of(nodes, gu, (size_t)cu), cen[recs[u].elem]);
+        const double score = is_deg ? 0.0 : face_score(normal, line);
+        double* slot = &boundary[recs[u].elem];
+        *slot = *slot < 0.0 ? score : (*slot < score ? *slot : score);
+        if (is_deg) degen[recs[u].elem] = 1;
+      }
+    }
+    i = j;
+  }
+  double sum = 0.0, mn = 90.0;
+  size_t ndeg = 0;
+  for (size_t e = 0; e < n_elem; ++e) {
+    double score = internal[e] >= 0.0 ? internal[e] : boundary[e];
+    if (score < 0.0) score = 90.0;
+    if (degen[e]) {
+      score = 0.0;
+      ++ndeg;
+    }
+    out_scores[e] = score;
+    sum += score;
+    mn = mn < score ? mn : score; /* std::min(min_score, score) */
+  }
+  *out_min = mn;
+  *out_mean = sum / (double)n_elem;
+  *out_degenerate = ndeg;
+  free(recs);
+  free(cen);
+  free(internal);
+  free(boundary);
+  free(degen);
+  return 0;
+}

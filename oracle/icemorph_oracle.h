@@ -78,6 +78,13 @@ int or_signed_measures(const double* nodes, size_t n_nodes, int dim, const int* 
                        const size_t* offsets, const size_t* conn, size_t n_elem, double* out,
                        size_t* inverted);
 
+/* quality.cpp:150-236 orthogonality: per-element scores (degrees) and
+ * signed measures, min / mean score, inverted and degenerate counts. */
+int or_orthogonality(const double* nodes, size_t n_nodes, int dim, const int* kinds,
+                     const size_t* offsets, const size_t* conn, size_t n_elem, double* out_scores,
+                     double* out_measures, double* out_min, double* out_mean,
+                     size_t* out_inverted, size_t* out_degenerate);
+
 #ifdef __cplusplus
 }
 #endif

@@ -254,6 +254,24 @@ class Oracle:
                       len(k), _dp(out), C.byref(inv)))
         return out[:len(k)].copy(), int(inv.value)
 
+    def orthogonality(self, nodes, dim, elements):
+        """quality.cpp:150-236: dict(scores, measures, min, mean, inverted, degenerate)."""
+        nodes = _xyz(nodes)
+        k, o, c = elements
+        k = np.ascontiguousarray(k, np.int32)
+        o = np.ascontiguousarray(o, np.uint64)
+        c = np.ascontiguousarray(c if len(c) else [0], np.uint64)
+        sc, me = np.zeros(max(len(k), 1)), np.zeros(max(len(k), 1))
+        mn, mean = _d(), _d()
+        inv, deg = _sz(), _sz()
+        f = self._fn("orthogonality")
+        f.argtypes = [_pd, _sz, C.c_int, _pi, _psz, _psz, _sz, _pd, _pd, C.POINTER(_d),
+                      C.POINTER(_d), _psz, _psz]
+        self._check(f(_dp(nodes), len(nodes), dim, k.ctypes.data_as(_pi), _szp(o), _szp(c), len(k),
+                      _dp(sc), _dp(me), C.byref(mn), C.byref(mean), C.byref(inv), C.byref(deg)))
+        return dict(scores=sc[:len(k)].copy(), measures=me[:len(k)].copy(), min=mn.value,
+                    mean=mean.value, inverted=int(inv.value), degenerate=int(deg.value))
+
     def deform(self, nodes, dim, patch, disp, pinned=(), tol=0.1, max_levels=5, cap=5000,
                kind="c2", R=1.0, volume_k=5.0, elements=None):
         """Reference deform() (ref flavour only).  With ``elements`` (CSR

@@ -397,3 +397,23 @@ extern "C" int ref_signed_measures(const double* nodes, size_t n_nodes, int dim,
     *inverted = count_inverted(m);  // quality.cpp:142-148
   });
 }
+
+// orthogonality (quality.cpp:150-236): per-element scores and measures, and
+// the report scalars {min, mean, inverted_count, degenerate_count}.
+extern "C" int ref_orthogonality(const double* nodes, size_t n_nodes, int dim, const int* kinds,
+                                 const size_t* offsets, const size_t* conn, size_t n_elem,
+                                 double* out_scores, double* out_measures, double* out_min,
+                                 double* out_mean, size_t* out_inverted, size_t* out_degenerate) {
+  return guarded([&] {
+    const Mesh m = mesh_with_elements(nodes, n_nodes, dim, kinds, offsets, conn, n_elem);
+    const QualityReport q = orthogonality(m);
+    if (n_elem) {
+      std::memcpy(out_scores, q.element_orthogonality_deg.data(), n_elem * sizeof(double));
+      std::memcpy(out_measures, q.element_signed_measure.data(), n_elem * sizeof(double));
+    }
+    *out_min = q.min_orthogonality_deg;
+    *out_mean = q.mean_orthogonality_deg;
+    *out_inverted = q.inverted_count;
+    *out_degenerate = q.degenerate_count;
+  });
+}

@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libicemorph_b200.so")
+LIB_PATH = os.environ.get("IMB_LIB") or os.path.join(HERE, "libicemorph_b200.so")  # IMB_LIB: development override
 KINDS = {"c0": 0, "c2": 1, "c4": 2, "c6": 3}
 PSI = {"linear": 0, "c2": 1, "wendland_c2": 1}
 EXACT, FP64 = 0, 1
@@ -57,7 +57,13 @@ class DeformConfigC(C.Structure):
     _fields_ = [("greedy", GreedyConfigC), ("volume_k", C.c_double),
                 ("support_distance", C.c_double), ("psi_kind", C.c_int), ("precision", C.c_int),
                 ("element_kinds", C.POINTER(C.c_int)), ("element_offsets", C.POINTER(C.c_size_t)),
-                ("element_nodes", C.POINTER(C.c_size_t)), ("n_elements", C.c_size_t)]
+                ("element_nodes", C.POINTER(C.c_size_t)), ("n_elements", C.c_size_t),
+                ("compute_quality", C.c_int)]
+
+
+class QualityReportC(C.Structure):
+    _fields_ = [("min_orthogonality_deg", C.c_double), ("mean_orthogonality_deg", C.c_double),
+                ("inverted_count", C.c_size_t), ("degenerate_count", C.c_size_t)]
 
 
 class DeformReportC(C.Structure):
@@ -65,7 +71,8 @@ class DeformReportC(C.Structure):
                 ("surface_max_error", C.c_double), ("surface_mean_error", C.c_double),
                 ("total_seconds", C.c_double), ("greedy_seconds", C.c_double),
                 ("distance_seconds", C.c_double), ("volume_seconds", C.c_double),
-                ("inverted_elements", C.c_size_t)]
+                ("inverted_elements", C.c_size_t), ("has_quality", C.c_int),
+                ("quality_before", QualityReportC), ("quality_after", QualityReportC)]
 
 
 _lib = None
@@ -91,7 +98,7 @@ EXPORTS = [
     "im_context_create", "im_context_destroy", "im_last_error", "im_last_device_ms",
     "im_version", "im_eval_wendland", "im_eval_basis", "im_make_wall_function",
     "im_eval_wall_function", "im_solve_weights", "im_eval_interpolant", "im_greedy_level",
-    "im_run_multilevel", "im_build_distance_index", "im_signed_measures", "im_count_inverted", "im_update_volume", "im_deform",
+    "im_run_multilevel", "im_build_distance_index", "im_signed_measures", "im_count_inverted", "im_orthogonality", "im_update_volume", "im_deform",
     "im_volume_plan_create", "im_volume_plan_destroy", "im_volume_plan_set_controls",
     "im_volume_plan_run", "im_volume_plan_reset_field", "im_volume_plan_download_field",
     "im_volume_plan_distances", "im_volume_plan_set_level", "im_volume_plan_run_steps",
@@ -123,6 +130,8 @@ def _declare(L):
     L.im_build_distance_index.argtypes = [C.c_void_p, _pd, _sz, C.c_int, _psz, _sz, _pd]
     L.im_signed_measures.argtypes = [C.c_void_p, _pd, _sz, _pi, _psz, _psz, _sz, _pd, _psz]
     L.im_count_inverted.argtypes = [C.c_void_p, _pd, _sz, _pi, _psz, _psz, _sz, _psz]
+    L.im_orthogonality.argtypes = [C.c_void_p, _pd, _sz, _pi, _psz, _psz, _sz, _pd, _pd,
+                                   C.POINTER(QualityReportC)]
     L.im_update_volume.argtypes = [C.c_void_p, _pd, _sz, _pd, _pd, _pd, _sz,
                                    C.POINTER(WallFunctionC), Basis, C.c_int, _psz, _pd, _psz]
     L.im_deform.argtypes = [C.c_void_p, _pd, _sz, C.c_int, _psz, _sz, _pd, _psz, _sz,
@@ -357,9 +366,23 @@ class Context:
             C.byref(inv)))
         return int(inv.value)
 
+    def orthogonality(self, nodes, elements):
+        """quality.cpp:150-236 on the device: dict(scores, measures, min, mean,
+        inverted, degenerate)."""
+        nodes = xyz(nodes)
+        k, o, c = elements
+        sc, me = np.zeros(max(len(k), 1)), np.zeros(max(len(k), 1))
+        rep = QualityReportC()
+        self._check(self.lib.im_orthogonality(
+            self.h, _dp(nodes), len(nodes), k.ctypes.data_as(_pi), _szp(o), _szp(c), len(k),
+            _dp(sc), _dp(me), C.byref(rep)))
+        return dict(scores=sc[:len(k)].copy(), measures=me[:len(k)].copy(),
+                    min=rep.min_orthogonality_deg, mean=rep.mean_orthogonality_deg,
+                    inverted=int(rep.inverted_count), degenerate=int(rep.degenerate_count))
+
     def deform(self, nodes, dim, patch, disp, pinned=(), tol=0.1, max_levels=5, cap=5000,
                kind="c2", R=1.0, volume_k=5.0, support_distance=-1.0, psi_kind=0,
-               precision=FP64, elements=None):
+               precision=FP64, elements=None, compute_quality=False):
         nodes, disp = xyz(nodes), xyz(disp)
         patch = np.ascontiguousarray(patch, dtype=np.uint64)
         pinned = np.ascontiguousarray(np.asarray(pinned, dtype=np.uint64).reshape(-1))
@@ -371,6 +394,7 @@ class Context:
             cfg.element_offsets = _szp(eo)
             cfg.element_nodes = _szp(ec)
             cfg.n_elements = len(ek)
+            cfg.compute_quality = int(bool(compute_quality))
         rep = DeformReportC()
         out = np.zeros_like(nodes)
         L = max_levels
@@ -389,7 +413,11 @@ class Context:
                     target_max=rep.target_max, surface_max_error=rep.surface_max_error,
                     surface_mean_error=rep.surface_mean_error, total_seconds=rep.total_seconds,
                     greedy_seconds=rep.greedy_seconds, distance_seconds=rep.distance_seconds,
-                    volume_seconds=rep.volume_seconds, inverted_elements=rep.inverted_elements)
+                    volume_seconds=rep.volume_seconds, inverted_elements=rep.inverted_elements,
+                    quality=None if not rep.has_quality else tuple(
+                        dict(min=q.min_orthogonality_deg, mean=q.mean_orthogonality_deg,
+                             inverted=int(q.inverted_count), degenerate=int(q.degenerate_count))
+                        for q in (rep.quality_before, rep.quality_after)))
 
 
 ELEMENT_KINDS = ("line", "triangle", "quadrilateral", "tetrahedron", "hexahedron", "prism",

@@ -9,8 +9,8 @@
 // Additive fields (defaults reproduce the reference): WallFunction::psi_kind,
 // DeformationConfig::{support_distance, psi_kind, precision}.  Out of scope
 // (not on the hot path): mesh I/O, generators, the orthogonality report;
-// DeformationReport carries inverted_elements but no QualityReport
-// (compute_quality is accepted and ignored).
+// DeformationReport carries inverted_elements and, with compute_quality and
+// mesh elements, the quality reports before / after (scalars only).
 #pragma once
 
 #include <cmath>
@@ -171,7 +171,7 @@ struct DeformationConfig {
   GreedyConfig greedy;
   double volume_k = 5.0;
   std::vector<std::string> fixed_markers;
-  bool compute_quality = true;  // accepted; quality metrics are out of scope
+  bool compute_quality = true;  // orthogonality before / after (device), needs elements
   // additive: absolute support distance (< 0: reference D_l = volume_k * target_max_l),
   // taper kind, arithmetic (0 exact reference order, 1 FP64 fast path)
   double support_distance = -1.0;
@@ -188,6 +188,17 @@ struct LevelSummary {
   double seconds = 0.0;
   ConvergenceRecord record;
 };
+// ---- quality.hpp ------------------------------------------------------------------
+struct QualityReport {
+  std::vector<double> element_orthogonality_deg;
+  std::vector<double> element_signed_measure;
+  double min_orthogonality_deg = 90.0;
+  double mean_orthogonality_deg = 90.0;
+  std::size_t inverted_count = 0;
+  std::size_t degenerate_count = 0;
+};
+QualityReport orthogonality(const Mesh& mesh);
+
 struct DeformationReport {
   std::string marker;
   std::vector<LevelSummary> levels;
@@ -195,6 +206,8 @@ struct DeformationReport {
   double surface_max_error = 0.0;
   double surface_mean_error = 0.0;
   std::size_t inverted_elements = 0;
+  std::optional<QualityReport> quality_before;  // element vectors left empty
+  std::optional<QualityReport> quality_after;
   double total_seconds = 0.0;
   std::size_t total_control_points() const;
 };

@@ -268,6 +268,23 @@ double signed_measure(const Mesh& mesh, const Element& element) {
 
 std::size_t count_inverted(const Mesh& mesh) { return measures(mesh, mesh.elements, nullptr); }
 
+QualityReport orthogonality(const Mesh& mesh) {
+  const ElementCsr csr(mesh.elements);
+  QualityReport q;
+  const std::size_t n = mesh.elements.size();
+  q.element_orthogonality_deg.resize(n);
+  q.element_signed_measure.resize(n);
+  im_quality_report r{};
+  check(im_orthogonality(ctx(), xyz(mesh.nodes), mesh.nodes.size(), csr.kinds.data(),
+                         csr.offsets.data(), csr.conn(), n, q.element_orthogonality_deg.data(),
+                         q.element_signed_measure.data(), &r));
+  q.min_orthogonality_deg = r.min_orthogonality_deg;
+  q.mean_orthogonality_deg = r.mean_orthogonality_deg;
+  q.inverted_count = r.inverted_count;
+  q.degenerate_count = r.degenerate_count;
+  return q;
+}
+
 std::pair<Mesh, DeformationReport> deform(const Mesh& mesh, const DisplacementField& disp,
                                           const DeformationConfig& config) {
   const Marker& marker = mesh.marker(disp.patch);
@@ -279,9 +296,16 @@ std::pair<Mesh, DeformationReport> deform(const Mesh& mesh, const DisplacementFi
   std::vector<Vec3> d(marker.nodes.size());
   for (std::size_t i = 0; i < marker.nodes.size(); ++i) d[i] = disp.at(marker.nodes[i]);
   const ElementCsr csr(mesh.elements);
-  const im_deform_config cfg{to_c(config.greedy), config.volume_k, config.support_distance,
-                             config.psi_kind,      config.precision, csr.kinds.data(),
-                             csr.offsets.data(),   csr.conn(),       mesh.elements.size()};
+  const im_deform_config cfg{to_c(config.greedy),
+                             config.volume_k,
+                             config.support_distance,
+                             config.psi_kind,
+                             config.precision,
+                             csr.kinds.data(),
+                             csr.offsets.data(),
+                             csr.conn(),
+                             mesh.elements.size(),
+                             config.compute_quality && !mesh.elements.empty() ? 1 : 0};
   Mesh out = mesh;
   im_deform_report rep{};
   const std::size_t L = std::max<std::size_t>(1, config.greedy.max_levels);
@@ -309,6 +333,18 @@ std::pair<Mesh, DeformationReport> deform(const Mesh& mesh, const DisplacementFi
   r.surface_max_error = rep.surface_max_error;
   r.surface_mean_error = rep.surface_mean_error;
   r.inverted_elements = rep.inverted_elements;
+  if (rep.has_quality) {
+    auto to_q = [](const im_quality_report& x) {
+      QualityReport q;
+      q.min_orthogonality_deg = x.min_orthogonality_deg;
+      q.mean_orthogonality_deg = x.mean_orthogonality_deg;
+      q.inverted_count = x.inverted_count;
+      q.degenerate_count = x.degenerate_count;
+      return q;
+    };
+    r.quality_before = to_q(rep.quality_before);
+    r.quality_after = to_q(rep.quality_after);
+  }
   r.total_seconds = rep.total_seconds;
   return {std::move(out), std::move(r)};
 }

@@ -415,6 +415,23 @@ int im_signed_measures(im_context* ctx, const double* nodes, size_t n_nodes, con
   });
 }
 
+int im_orthogonality(im_context* ctx, const double* nodes, size_t n_nodes, const int* kinds,
+                     const size_t* offsets, const size_t* conn, size_t n_elem, double* scores,
+                     double* measures, im_quality_report* rep) {
+  return guarded(ctx, [&](Context& c) {
+    DPoints dn;
+    upload_points(c, nodes, n_nodes, dn);
+    EventTimer tm(c.stream);
+    const QualityStats q = orthogonality_from_host(c, dn.x.p, dn.y.p, dn.z.p, n_nodes, kinds, offsets,
+                                                   conn, n_elem, scores, measures);
+    c.last_kernel_ms = tm.stop();
+    rep->min_orthogonality_deg = q.min_deg;
+    rep->mean_orthogonality_deg = q.mean_deg;
+    rep->inverted_count = q.inverted;
+    rep->degenerate_count = q.degenerate;
+  });
+}
+
 int im_count_inverted(im_context* ctx, const double* nodes, size_t n_nodes, const int* kinds,
                       const size_t* offsets, const size_t* conn, size_t n_elem, size_t* inverted) {
   return im_signed_measures(ctx, nodes, n_nodes, kinds, offsets, conn, n_elem, nullptr, inverted);

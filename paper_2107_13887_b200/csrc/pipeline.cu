@@ -378,12 +378,30 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
       if (level_seconds) level_seconds[l] = lv.seconds;
     }
     c.last_kernel_ms = tm.ms();
-    // count_inverted(deformed) (pipeline.cpp:101) on the resident deformed nodes
+    // count_inverted(deformed) (pipeline.cpp:101) on the resident deformed nodes,
+    // and the quality reports before / after (pipeline.cpp:55, 102)
     rep->inverted_elements = 0;
-    if (cfg->n_elements)
-      rep->inverted_elements = signed_measures_from_host(
-          c, acc.x.p, acc.y.p, acc.z.p, n_nodes, cfg->element_kinds, cfg->element_offsets,
-          cfg->element_nodes, cfg->n_elements, nullptr);
+    rep->has_quality = 0;
+    if (cfg->n_elements) {
+      if (cfg->compute_quality) {
+        auto to_rep = [](const QualityStats& q) {
+          return im_quality_report{q.min_deg, q.mean_deg, q.inverted, q.degenerate};
+        };
+        rep->quality_before = to_rep(orthogonality_from_host(
+            c, dn.x.p, dn.y.p, dn.z.p, n_nodes, cfg->element_kinds, cfg->element_offsets,
+            cfg->element_nodes, cfg->n_elements, nullptr, nullptr));
+        const QualityStats after = orthogonality_from_host(
+            c, acc.x.p, acc.y.p, acc.z.p, n_nodes, cfg->element_kinds, cfg->element_offsets,
+            cfg->element_nodes, cfg->n_elements, nullptr, nullptr);
+        rep->quality_after = to_rep(after);
+        rep->inverted_elements = after.inverted;
+        rep->has_quality = 1;
+      } else {
+        rep->inverted_elements = signed_measures_from_host(
+            c, acc.x.p, acc.y.p, acc.z.p, n_nodes, cfg->element_kinds, cfg->element_offsets,
+            cfg->element_nodes, cfg->n_elements, nullptr);
+      }
+    }
     DBuf<double> aos;
     aos.reserve(3 * n_nodes);
     k_soa_to_aos<<<(n_nodes + 255) / 256, 256, 0, c.stream>>>(acc.x.p, acc.y.p, acc.z.p, n_nodes,

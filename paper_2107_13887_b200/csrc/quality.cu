@@ -19,7 +19,11 @@
 // validate_mesh, mesh.cpp:162-186) are reported through an atomicMin on the
 // first offending element so the host can raise the reference's message.
 #include <cstdio>
+#include <cstring>
 #include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
 
 #include "common.cuh"
 #include "runtime.hpp"
@@ -228,6 +232,297 @@ size_t signed_measures_from_host(Context& ctx, const double* x, const double* y,
   const size_t inverted = signed_measures(ctx, x, y, z, n_nodes, dk, doff, dconn, n_elem, dout);
   if (out && n_elem) IMB_CHECK(cudaMemcpy(out, dout, n_elem * 8, cudaMemcpyDeviceToHost));
   return inverted;
+}
+
+}  // namespace imb
+
+// ---- orthogonality (quality.cpp:150-236) --------------------------------------
+// Face matching without the reference's std::map: every element emits its
+// faces (element_faces, quality.cpp:19-49) as records keyed by the sorted
+// global node ids (two 64-bit words), a stable two-pass radix sort groups
+// equal keys with their uses in element-major order (= the map's per-key
+// vector order), and one thread per group applies quality.cpp:178-200.
+// Per-element folds use integer atomicMin on the (non-negative) score bits.
+// All vector arithmetic follows vec.hpp with explicit IEEE ops; atan2 is
+// CUDA's (<= 2 ulp), so scores agree with the reference to ~1e-13 degrees,
+// not bit for bit.  The mean is summed on the host in element order.
+namespace imb {
+namespace {
+
+__constant__ int kFaceCnt[7] = {0, 3, 4, 4, 6, 5, 5};
+__constant__ unsigned char kFaceTab[7][6][5] = {
+    {{0}},
+    {{2, 0, 1}, {2, 1, 2}, {2, 2, 0}},
+    {{2, 0, 1}, {2, 1, 2}, {2, 2, 3}, {2, 3, 0}},
+    {{3, 0, 1, 2}, {3, 0, 1, 3}, {3, 1, 2, 3}, {3, 0, 2, 3}},
+    {{4, 0, 1, 2, 3}, {4, 4, 5, 6, 7}, {4, 0, 1, 5, 4}, {4, 1, 2, 6, 5}, {4, 2, 3, 7, 6},
+     {4, 3, 0, 4, 7}},
+    {{3, 0, 1, 2}, {3, 3, 4, 5}, {4, 0, 1, 4, 3}, {4, 1, 2, 5, 4}, {4, 2, 0, 3, 5}},
+    {{4, 0, 1, 2, 3}, {3, 0, 1, 4}, {3, 1, 2, 4}, {3, 2, 3, 4}, {3, 3, 0, 4}},
+};
+
+struct D3 {
+  double x, y, z;
+};
+__device__ __forceinline__ D3 dsub3(D3 a, D3 b) { return {sub(a.x, b.x), sub(a.y, b.y), sub(a.z, b.z)}; }
+__device__ __forceinline__ D3 dadd3(D3 a, D3 b) { return {add(a.x, b.x), add(a.y, b.y), add(a.z, b.z)}; }
+__device__ __forceinline__ D3 dscale3(D3 a, double s) { return {mul(a.x, s), mul(a.y, s), mul(a.z, s)}; }
+__device__ __forceinline__ double dsq3(D3 a) { return add(add(mul(a.x, a.x), mul(a.y, a.y)), mul(a.z, a.z)); }
+__device__ __forceinline__ double ddot3(D3 a, D3 b) { return add(add(mul(a.x, b.x), mul(a.y, b.y)), mul(a.z, b.z)); }
+__device__ __forceinline__ D3 dcross3(D3 a, D3 b) {
+  return {sub(mul(a.y, b.z), mul(a.z, b.y)), sub(mul(a.z, b.x), mul(a.x, b.z)),
+          sub(mul(a.x, b.y), mul(a.y, b.x))};
+}
+// vec.hpp:64-67
+__device__ __forceinline__ D3 dnormalized(D3 v) {
+  const double n = __dsqrt_rn(dsq3(v));
+  return n > 0.0 ? dscale3(v, __ddiv_rn(1.0, n)) : D3{0.0, 0.0, 0.0};
+}
+
+struct Geo {
+  const double *x, *y, *z;
+  const int* kinds;
+  const unsigned long long *offsets, *conn;
+  __device__ D3 node(unsigned long long i) const { return {x[i], y[i], z[i]}; }
+  // global nodes of local face f of element e, in the face's own order
+  __device__ int face(unsigned long long e, int f, unsigned long long (&g)[4]) const {
+    const unsigned char* t = kFaceTab[kinds[e]][f];
+    for (int k = 0; k < t[0]; ++k) g[k] = conn[offsets[e] + t[1 + k]];
+    return t[0];
+  }
+};
+
+// quality.cpp:51-55 / 74-78: node sum in order, times 1/count
+__device__ D3 centroid(const Geo& G, const unsigned long long* g, int cnt) {
+  D3 c{0.0, 0.0, 0.0};
+  for (int k = 0; k < cnt; ++k) c = dadd3(c, G.node(g[k]));
+  return dscale3(c, __ddiv_rn(1.0, (double)cnt));
+}
+
+// quality.cpp:57-72
+__device__ D3 face_normal(const Geo& G, const unsigned long long (&g)[4], int cnt) {
+  if (cnt == 2) {
+    const D3 t = dsub3(G.node(g[1]), G.node(g[0]));
+    return dnormalized({t.y, -t.x, 0.0});
+  }
+  const D3 a = G.node(g[0]), b = G.node(g[1]), c = G.node(g[2]);
+  D3 n = dcross3(dsub3(b, a), dsub3(c, a));
+  if (cnt == 4) n = dadd3(dnormalized(n), dnormalized(dcross3(dsub3(c, a), dsub3(G.node(g[3]), a))));
+  return dnormalized(n);
+}
+
+// quality.cpp:82-88
+__device__ double face_score(D3 normal, D3 line) {
+  const D3 c = dnormalized(line);
+  if (dsq3(normal) == 0.0 || dsq3(c) == 0.0) return 0.0;
+  const double along = fabs(ddot3(normal, c));
+  const double transverse = __dsqrt_rn(dsq3(dcross3(normal, c)));
+  return sub(90.0, __ddiv_rn(mul(atan2(transverse, along), 180.0), 3.141592653589793));
+}
+
+__global__ void k_face_counts(const int* kinds, size_t n, unsigned* cnt) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) cnt[e] = (unsigned)kFaceCnt[kinds[e]];
+}
+
+__global__ void k_face_keys(Geo G, size_t n, const unsigned long long* foff,
+                            unsigned long long* khi, unsigned long long* klo, unsigned* ef,
+                            unsigned* vals) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int nf = kFaceCnt[G.kinds[e]];
+  for (int f = 0; f < nf; ++f) {
+    unsigned long long g[4];
+    const int c = G.face(e, f, g);
+    unsigned s[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+    for (int k = 0; k < c; ++k) s[k] = (unsigned)g[k];
+    for (int a = 1; a < c; ++a)
+      for (int b = a; b > 0 && s[b - 1] > s[b]; --b) {
+        const unsigned t = s[b];
+        s[b] = s[b - 1], s[b - 1] = t;
+      }
+    const size_t r = foff[e] + f;
+    khi[r] = ((unsigned long long)s[0] << 32) | s[1];
+    klo[r] = ((unsigned long long)s[2] << 32) | s[3];
+    ef[r] = (unsigned)(e * 8 + f);
+    vals[r] = (unsigned)r;
+  }
+}
+
+__global__ void k_gather_u64(const unsigned long long* src, const unsigned* idx, size_t n,
+                             unsigned long long* dst) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
+__global__ void k_centroids(Geo G, size_t n, double* cx, double* cy, double* cz) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  D3 c{0.0, 0.0, 0.0};
+  const unsigned long long o = G.offsets[e], cnt = G.offsets[e + 1] - o;
+  for (unsigned long long k = 0; k < cnt; ++k) c = dadd3(c, G.node(G.conn[o + k]));
+  c = dscale3(c, __ddiv_rn(1.0, (double)cnt));
+  cx[e] = c.x, cy[e] = c.y, cz[e] = c.z;
+}
+
+__device__ __forceinline__ void fold_min(unsigned long long* slot, double v) {
+  atomicMin(slot, (unsigned long long)__double_as_longlong(v));  // v >= 0: bit order == value order
+}
+
+// one thread per sorted face position; the first position of each key group
+// handles the group (quality.cpp:178-200)
+__global__ void k_face_groups(Geo G, size_t nf, const unsigned* order, const unsigned long long* khi,
+                              const unsigned long long* klo, const unsigned* ef,
+                              const double* cx, const double* cy, const double* cz,
+                              unsigned long long* internal, unsigned long long* boundary,
+                              unsigned* degenerate) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nf) return;
+  const unsigned r0 = order[i];
+  const unsigned long long h = khi[r0], l = klo[r0];
+  if (i > 0 && khi[order[i - 1]] == h && klo[order[i - 1]] == l) return;
+  size_t j = i + 1;
+  while (j < nf && khi[order[j]] == h && klo[order[j]] == l) ++j;
+  unsigned long long g0[4];
+  const unsigned u0 = ef[r0];
+  const int cnt = G.face(u0 >> 3, u0 & 7, g0);
+  const D3 normal = face_normal(G, g0, cnt);  // uses.front().global
+  const bool deg = dsq3(normal) == 0.0;
+  if (j - i == 2) {
+    const unsigned e0 = ef[order[i]] >> 3, e1 = ef[order[i + 1]] >> 3;
+    const D3 line = dsub3(D3{cx[e1], cy[e1], cz[e1]}, D3{cx[e0], cy[e0], cz[e0]});
+    const double score = deg ? 0.0 : face_score(normal, line);
+    for (size_t u = i; u < j; ++u) {
+      const unsigned e = ef[order[u]] >> 3;
+      fold_min(&internal[e], score);
+      if (deg) atomicOr(&degenerate[e], 1u);
+    }
+  } else {
+    for (size_t u = i; u < j; ++u) {
+      const unsigned uu = ef[order[u]], e = uu >> 3;
+      unsigned long long g[4];
+      const int c = G.face(e, uu & 7, g);
+      const D3 line = dsub3(centroid(G, g, c), D3{cx[e], cy[e], cz[e]});
+      const double score = deg ? 0.0 : face_score(normal, line);
+      fold_min(&boundary[e], score);
+      if (deg) atomicOr(&degenerate[e], 1u);
+    }
+  }
+}
+
+// quality.cpp:215-224 per element
+__global__ void k_element_scores(size_t n, const unsigned long long* internal,
+                                 const unsigned long long* boundary, const unsigned* degenerate,
+                                 double* scores) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const unsigned long long unset = 0x7ff0000000000000ull;  // +inf: no face of that kind
+  double s = internal[e] != unset ? __longlong_as_double((long long)internal[e])
+           : boundary[e] != unset ? __longlong_as_double((long long)boundary[e]) : 90.0;
+  if (degenerate[e]) s = 0.0;
+  scores[e] = s;
+}
+
+__global__ void k_fill_u64(unsigned long long* p, size_t n, unsigned long long v) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+}  // namespace
+
+QualityStats orthogonality_device(Context& ctx, const double* x, const double* y, const double* z,
+                                  size_t n_nodes, const int* kinds, const unsigned long long* offsets,
+                                  const unsigned long long* conn, size_t n_elem, double* scores,
+                                  double* measures) {
+  QualityStats q;
+  // signed measures + validation (also rejects malformed elements)
+  q.inverted = signed_measures(ctx, x, y, z, n_nodes, kinds, offsets, conn, n_elem, measures);
+  if (n_elem == 0) return q;
+  if (n_elem >= (size_t(1) << 29) || n_nodes >= 0xffffffffull)
+    throw InvalidArgument("orthogonality: mesh too large (elements < 2^29, nodes < 2^32)");
+  const Geo G{x, y, z, kinds, offsets, conn};
+  const unsigned nb = (unsigned)((n_elem + 255) / 256);
+  DBuf<unsigned> cnt;
+  DBuf<unsigned long long> foff;
+  cnt.reserve(n_elem);
+  foff.reserve(n_elem + 1);
+  k_face_counts<<<nb, 256, 0, ctx.stream>>>(kinds, n_elem, cnt.p);
+  scan_u32_to_u64_async(ctx, cnt.p, n_elem, foff.p);
+  unsigned long long nf_h = 0;
+  IMB_CHECK(cudaMemcpyAsync(&nf_h, foff.p + n_elem, 8, cudaMemcpyDeviceToHost, ctx.stream));
+  IMB_CHECK(cudaStreamSynchronize(ctx.stream));
+  const size_t nf = (size_t)nf_h;
+  if (nf >= 0xffffffffull) throw InvalidArgument("orthogonality: too many faces");
+  DBuf<unsigned long long> khi, klo, ks, kg;
+  DBuf<unsigned> ef, v0, v1, v2;
+  for (auto* b : {&khi, &klo, &ks, &kg}) b->reserve(std::max<size_t>(nf, 1));
+  for (auto* b : {&ef, &v0, &v1, &v2}) b->reserve(std::max<size_t>(nf, 1));
+  k_face_keys<<<nb, 256, 0, ctx.stream>>>(G, n_elem, foff.p, khi.p, klo.p, ef.p, v0.p);
+  // stable LSD: by the low key word, then by the high word
+  size_t t1 = 0, t2 = 0;
+  IMB_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, t1, klo.p, ks.p, v0.p, v1.p, (int)nf, 0, 64, ctx.stream));
+  IMB_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, t2, kg.p, ks.p, v1.p, v2.p, (int)nf, 0, 64, ctx.stream));
+  DBuf<unsigned char> tmp;
+  tmp.reserve(std::max(t1, t2));
+  IMB_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, t1, klo.p, ks.p, v0.p, v1.p, (int)nf, 0, 64, ctx.stream));
+  const unsigned fb = (unsigned)((nf + 255) / 256);
+  k_gather_u64<<<fb, 256, 0, ctx.stream>>>(khi.p, v1.p, nf, kg.p);
+  IMB_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, t2, kg.p, ks.p, v1.p, v2.p, (int)nf, 0, 64, ctx.stream));
+  DBuf<double> cx, cy, cz;
+  cx.reserve(n_elem), cy.reserve(n_elem), cz.reserve(n_elem);
+  k_centroids<<<nb, 256, 0, ctx.stream>>>(G, n_elem, cx.p, cy.p, cz.p);
+  DBuf<unsigned long long> in_s, bd_s;
+  DBuf<unsigned> deg;
+  in_s.reserve(n_elem), bd_s.reserve(n_elem), deg.reserve(n_elem);
+  k_fill_u64<<<nb, 256, 0, ctx.stream>>>(in_s.p, n_elem, 0x7ff0000000000000ull);
+  k_fill_u64<<<nb, 256, 0, ctx.stream>>>(bd_s.p, n_elem, 0x7ff0000000000000ull);
+  IMB_CHECK(cudaMemsetAsync(deg.p, 0, n_elem * 4, ctx.stream));
+  k_face_groups<<<fb, 256, 0, ctx.stream>>>(G, nf, v2.p, khi.p, klo.p, ef.p, cx.p, cy.p, cz.p,
+                                            in_s.p, bd_s.p, deg.p);
+  DBuf<double> sc;
+  sc.reserve(n_elem);
+  k_element_scores<<<nb, 256, 0, ctx.stream>>>(n_elem, in_s.p, bd_s.p, deg.p, sc.p);
+  IMB_LAUNCH_CHECK();
+  std::vector<double> h(n_elem);
+  std::vector<unsigned> hd(n_elem);
+  IMB_CHECK(cudaMemcpyAsync(h.data(), sc.p, n_elem * 8, cudaMemcpyDeviceToHost, ctx.stream));
+  IMB_CHECK(cudaMemcpyAsync(hd.data(), deg.p, n_elem * 4, cudaMemcpyDeviceToHost, ctx.stream));
+  IMB_CHECK(cudaStreamSynchronize(ctx.stream));
+  // quality.cpp:225-234: in element order on the host (the reference's sum)
+  double sum = 0.0, mn = 90.0;
+  for (size_t e = 0; e < n_elem; ++e) {
+    sum += h[e];
+    mn = h[e] < mn ? h[e] : mn;
+    q.degenerate += hd[e] ? 1 : 0;
+  }
+  q.min_deg = mn;
+  q.mean_deg = sum / (double)n_elem;
+  if (scores) std::memcpy(scores, h.data(), n_elem * 8);
+  return q;
+}
+
+QualityStats orthogonality_from_host(Context& ctx, const double* x, const double* y, const double* z,
+                                     size_t n_nodes, const int* kinds, const size_t* offsets,
+                                     const size_t* conn, size_t n_elem, double* scores,
+                                     double* measures) {
+  if (n_elem && !(kinds && offsets && conn)) throw InvalidArgument("element arrays are null");
+  if (n_elem && offsets[0] != 0) throw InvalidArgument("element offsets must start at 0");
+  const size_t n_conn = n_elem ? offsets[n_elem] : 0;
+  int* dk = ctx.buf<int>(Context::kSlotElemKind, n_elem);
+  auto* doff = ctx.buf<unsigned long long>(Context::kSlotElemOffset, n_elem + 1);
+  auto* dconn = ctx.buf<unsigned long long>(Context::kSlotElemNodes, n_conn);
+  if (n_elem) {
+    IMB_CHECK(cudaMemcpyAsync(dk, kinds, n_elem * sizeof(int), cudaMemcpyHostToDevice, ctx.stream));
+    IMB_CHECK(cudaMemcpyAsync(doff, offsets, (n_elem + 1) * 8, cudaMemcpyHostToDevice, ctx.stream));
+    if (n_conn)
+      IMB_CHECK(cudaMemcpyAsync(dconn, conn, n_conn * 8, cudaMemcpyHostToDevice, ctx.stream));
+  }
+  DBuf<double> dm;
+  if (measures) dm.reserve(std::max<size_t>(n_elem, 1));
+  const QualityStats q = orthogonality_device(ctx, x, y, z, n_nodes, dk, doff, dconn, n_elem, scores,
+                                              measures ? dm.p : nullptr);
+  if (measures && n_elem) IMB_CHECK(cudaMemcpy(measures, dm.p, n_elem * 8, cudaMemcpyDeviceToHost));
+  return q;
 }
 
 }  // namespace imb

@@ -259,6 +259,21 @@ void scan_u32_to_u64(Context& ctx, const unsigned int* in, size_t n, unsigned lo
 size_t signed_measures(Context& ctx, const double* x, const double* y, const double* z,
                        size_t n_nodes, const int* kinds, const unsigned long long* offsets,
                        const unsigned long long* conn, size_t n_elem, double* out);
+// quality.cpp:150-236 orthogonality on the device (elements device CSR):
+// per-element scores (device pointer, may be null), signed measures (device
+// pointer, may be null), report scalars.
+struct QualityStats {
+  double min_deg = 90.0, mean_deg = 90.0;
+  size_t inverted = 0, degenerate = 0;
+};
+QualityStats orthogonality_device(Context& ctx, const double* x, const double* y, const double* z,
+                                  size_t n_nodes, const int* kinds, const unsigned long long* offsets,
+                                  const unsigned long long* conn, size_t n_elem, double* scores_host,
+                                  double* measures_device);
+QualityStats orthogonality_from_host(Context& ctx, const double* x, const double* y, const double* z,
+                                     size_t n_nodes, const int* kinds, const size_t* offsets,
+                                     const size_t* conn, size_t n_elem, double* scores,
+                                     double* measures);
 // Same with the element CSR (and out) on the host; uploads through context slots.
 size_t signed_measures_from_host(Context& ctx, const double* x, const double* y, const double* z,
                                  size_t n_nodes, const int* kinds, const size_t* offsets,

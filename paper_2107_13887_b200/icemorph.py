@@ -7,9 +7,10 @@ Same names, argument meaning and error behaviour as the reference binding:
 ``Mesh`` / ``DisplacementField`` / ``DeformationConfig`` / ``DeformationReport``
 / ``LevelSummary``; ``ValueError`` for std::invalid_argument and
 ``RuntimeError`` (``capi.SolveError``) for icemorph::SolveError, as pybind11
-maps them, plus ``signed_measures`` (bindings.cpp:195-197) and the report's
-``inverted_elements`` (pipeline.cpp:101) on the device.  Mesh I/O, generators
-and the orthogonality report are out of scope; a ``Mesh`` is built from
+maps them, plus ``orthogonality`` / ``signed_measures`` (bindings.cpp:194-197)
+and the report's ``inverted_elements`` / ``quality_before`` / ``quality_after``
+(pipeline.cpp:55, 101-102) on the device.  Mesh I/O and generators are out of
+scope; a ``Mesh`` is built from
 arrays (``Mesh(dim, nodes, markers, elements)``) instead of ``read_su2`` /
 ``gen_airfoil_mesh``.
 """
@@ -127,7 +128,7 @@ class DeformationConfig:
         self.max_points_per_level = 5000
         self.volume_k = 5.0
         self.fixed_markers: list[str] = []
-        self.compute_quality = True  # accepted; quality metrics are out of scope
+        self.compute_quality = True  # orthogonality before / after (needs mesh elements)
         self.support_distance = None
         self.psi = "linear"
         self.precision = "exact"
@@ -161,6 +162,24 @@ class DeformationReport:
         return sum(l.points for l in self.levels)
 
 
+@dataclass
+class QualityReport:
+    """bindings.cpp:128-134 (quality.hpp QualityReport)."""
+    min_orthogonality_deg: float = 90.0
+    mean_orthogonality_deg: float = 90.0
+    inverted_count: int = 0
+    degenerate_count: int = 0
+    element_orthogonality_deg: list = field(default_factory=list)
+    element_signed_measure: list = field(default_factory=list)
+
+
+def orthogonality(mesh: Mesh) -> QualityReport:
+    """bindings.cpp:194 -> orthogonality (quality.cpp:150-236), on the device."""
+    q = _context().orthogonality(mesh._nodes, mesh._elements)
+    return QualityReport(q["min"], q["mean"], q["inverted"], q["degenerate"],
+                         q["scores"].tolist(), q["measures"].tolist())
+
+
 def signed_measures(mesh: Mesh):
     """bindings.cpp:195-197 -> signed_measures (quality.cpp:135-140)."""
     return _context().signed_measures(mesh._nodes, mesh._elements)[0].tolist()
@@ -169,6 +188,13 @@ def signed_measures(mesh: Mesh):
 def count_inverted(mesh: Mesh) -> int:
     """count_inverted (quality.cpp:142-148)."""
     return _context().count_inverted(mesh._nodes, mesh._elements)
+
+
+def _quality(r, k):
+    q = r["quality"]
+    if q is None:
+        return None
+    return QualityReport(q[k]["min"], q[k]["mean"], q[k]["inverted"], q[k]["degenerate"])
 
 
 def deform(mesh: Mesh, displacement: DisplacementField, config: DeformationConfig):
@@ -185,12 +211,14 @@ def deform(mesh: Mesh, displacement: DisplacementField, config: DeformationConfi
                           config.support_radius, config.volume_k, D,
                           1 if config.psi in ("c2", "wendland_c2") else 0,
                           capi.EXACT if config.precision == "exact" else capi.FP64,
-                          elements=mesh._elements)
+                          elements=mesh._elements,
+                          compute_quality=config.compute_quality and mesh.num_elements > 0)
     out = Mesh(mesh.dim, r["nodes"], mesh._markers, mesh._elements)
     rep = DeformationReport(marker=displacement.patch, target_max=r["target_max"],
                             surface_max_error=r["surface_max_error"],
                             surface_mean_error=r["surface_mean_error"],
                             inverted_elements=int(r["inverted_elements"]),
+                            quality_before=_quality(r, 0), quality_after=_quality(r, 1),
                             total_seconds=r["total_seconds"])
     for l in range(len(r["points"])):
         rep.levels.append(LevelSummary(l, int(r["points"][l]), float(r["achieved"][l]),

@@ -122,6 +122,14 @@ int main() {
   CHECK(std::abs(signed_measure(cube, cube.elements[0]) - 1.0) < 1e-14);
   cube.elements[0].nodes = {4, 5, 7, 6, 0, 1, 3, 2};
   CHECK(count_inverted(cube) == 1);
+  // test_quality.cpp:22-34: two right triangles score 90 across the hypotenuse
+  Mesh tris;
+  tris.dim = 2;
+  tris.nodes = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0}};
+  tris.elements = {{ElementKind::Triangle, {0, 1, 2}}, {ElementKind::Triangle, {0, 2, 3}}};
+  const QualityReport q = orthogonality(tris);
+  CHECK(std::abs(q.element_orthogonality_deg[0] - 90.0) < 1e-10 &&
+        std::abs(q.element_orthogonality_deg[1] - 90.0) < 1e-10 && q.inverted_count == 0);
   std::printf(failures ? "shim: %d FAILED\n" : "shim: all passed\n", failures);
   return failures ? 1 : 0;
 }
