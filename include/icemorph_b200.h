@@ -37,6 +37,7 @@ extern "C" {
 #define IM_INVALID_ARGUMENT 1
 #define IM_SOLVE_ERROR 2
 #define IM_RUNTIME_ERROR 3
+#define IM_PARSE_ERROR 4 /* icemorph::ParseError (mesh_io.hpp:14-21); line: im_last_error_line */
 
 /* WendlandKind, rbf.hpp:18 */
 #define IM_C0 0
@@ -176,6 +177,32 @@ int im_orthogonality(im_context* ctx, const double* nodes, size_t n_nodes,
                      const int* element_kinds, const size_t* element_offsets,
                      const size_t* element_nodes, size_t n_elements, double* element_scores,
                      double* element_measures, im_quality_report* report);
+
+/* ---- SU2 mesh I/O (mesh_io.hpp:39-43, mesh_io.cpp:127-309) -------------------
+ * im_su2_read parses a SU2 ASCII mesh (NDIME / NPOIN / NELEM / NMARK, any
+ * order, '%' comments) into an opaque host mesh with the reference's grammar,
+ * validation and "path:line: what" errors (IM_PARSE_ERROR; the line via
+ * im_last_error_line), including the coincident-node check (on the device).
+ * Accessors copy the arrays out; element kinds are ElementKind ids
+ * (mesh.hpp:15-23).  im_su2_write writes the reference's layout (NDIME, NELEM,
+ * NPOIN with %.17g coordinates, NMARK). */
+typedef struct im_mesh im_mesh;
+int im_su2_read(im_context* ctx, const char* path, im_mesh** out);
+int im_mesh_destroy(im_mesh* mesh);
+int im_mesh_sizes(const im_mesh* mesh, int* dim, size_t* n_nodes, size_t* n_elements,
+                  size_t* n_element_nodes, size_t* n_markers);
+int im_mesh_nodes(const im_mesh* mesh, double* xyz);
+int im_mesh_elements(const im_mesh* mesh, int* kinds, size_t* offsets, size_t* nodes);
+int im_mesh_marker_sizes(const im_mesh* mesh, size_t marker, size_t* name_length,
+                         size_t* n_elements, size_t* n_element_nodes, size_t* n_nodes);
+int im_mesh_marker(const im_mesh* mesh, size_t marker, char* name, int* kinds, size_t* offsets,
+                   size_t* element_nodes, size_t* nodes);
+size_t im_last_error_line(const im_context* ctx);
+int im_su2_write(im_context* ctx, const char* path, int dim, const double* xyz, size_t n_nodes,
+                 const int* kinds, const size_t* offsets, const size_t* nodes, size_t n_elements,
+                 size_t n_markers, const char* const* marker_names, const int* const* marker_kinds,
+                 const size_t* const* marker_offsets, const size_t* const* marker_element_nodes,
+                 const size_t* marker_n_elements);
 
 /* ---- pipeline -----------------------------------------------------------------
  * deform, pipeline.hpp:54-56 (pipeline.cpp:19-106) on a mesh given as its

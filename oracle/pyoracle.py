@@ -254,6 +254,61 @@ class Oracle:
                       len(k), _dp(out), C.byref(inv)))
         return out[:len(k)].copy(), int(inv.value)
 
+    def read_su2(self, path: str) -> dict:
+        """Reference read_su2 (ref flavour only): same dict as capi.Context.read_su2;
+        a ParseError raises OracleError with .line set."""
+        assert self.flavour == "ref"
+        f = self.lib.ref_read_su2
+        f.argtypes = [C.c_char_p, _psz, _pd, _pi, _psz, _psz, C.c_char_p, _psz, _psz, _psz, _pi,
+                      _psz, _psz, _psz]
+        sizes = np.zeros(6, np.uint64)
+        big = np.zeros(1 << 16, np.uint64)  # per-marker counts (<= 65536 markers)
+        me, mc, mn = big.copy(), big.copy(), big.copy()
+        self._check_su2(f(os.fsencode(path), _szp(sizes), None, None, None, None, None, _szp(me),
+                          _szp(mc), _szp(mn), None, None, None, None))
+        dim, nn, ne, nc, nm, nb = (int(v) for v in sizes)
+        xyz = np.zeros((max(nn, 1), 3))
+        k = np.zeros(max(ne, 1), np.int32)
+        o = np.zeros(ne + 1, np.uint64)
+        c = np.zeros(max(nc, 1), np.uint64)
+        names = C.create_string_buffer(nb + 1)
+        tme, tmc, tmn = int(me[:nm].sum()), int(mc[:nm].sum()), int(mn[:nm].sum())
+        mk = np.zeros(max(tme, 1), np.int32)
+        mcnt = np.zeros(max(tme, 1), np.uint64)
+        mconn = np.zeros(max(tmc, 1), np.uint64)
+        mnodes = np.zeros(max(tmn, 1), np.uint64)
+        self._check_su2(f(os.fsencode(path), _szp(sizes), _dp(xyz), k.ctypes.data_as(_pi), _szp(o),
+                          _szp(c), names, _szp(me), _szp(mc), _szp(mn), mk.ctypes.data_as(_pi),
+                          _szp(mcnt), _szp(mconn), _szp(mnodes)))
+        markers, pe, pc, pn = [], 0, 0, 0
+        for i, name in enumerate(names.raw[:nb].decode().split("\n")[:nm]):
+            e, cc, nd = int(me[i]), int(mc[i]), int(mn[i])
+            offs = np.zeros(e + 1, np.uint64)
+            offs[1:] = np.cumsum(mcnt[pe:pe + e])
+            markers.append(dict(name=name, elements=(mk[pe:pe + e].copy(), offs, mconn[pc:pc + cc].copy()),
+                                nodes=mnodes[pn:pn + nd].astype(np.int64)))
+            pe, pc, pn = pe + e, pc + cc, pn + nd
+        return dict(dim=dim, nodes=xyz[:nn], elements=(k[:ne], o, c[:nc]), markers=markers)
+
+    def roundtrip_su2(self, src: str, dst: str):
+        """Reference write_su2(read_su2(src)) into dst, in a separate process
+        (oracle/_ref/ref_su2_tool): the reference's ostream writer must not run
+        in a process with numpy loaded."""
+        import subprocess
+
+        tool = os.path.join(HERE, "_ref", "ref_su2_tool")
+        r = subprocess.run([tool, "roundtrip", src, dst], capture_output=True, text=True)
+        if r.returncode:
+            raise OracleError(3, r.stderr.strip())
+
+    def _check_su2(self, rc):
+        if rc == 4:
+            e = OracleError(rc, self.lib.ref_last_error().decode())
+            self.lib.ref_last_error_line.restype = C.c_size_t
+            e.line = int(self.lib.ref_last_error_line())
+            raise e
+        self._check(rc)
+
     def orthogonality(self, nodes, dim, elements):
         """quality.cpp:150-236: dict(scores, measures, min, mean, inverted, degenerate)."""
         nodes = _xyz(nodes)

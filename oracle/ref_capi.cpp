@@ -38,6 +38,7 @@
 #include <vector>
 
 #include "icemorph/greedy.hpp"
+#include "icemorph/mesh_io.hpp"
 #include "icemorph/pipeline.hpp"
 #include "icemorph/quality.hpp"
 #include "icemorph/rbf.hpp"
@@ -48,6 +49,7 @@ using namespace icemorph;
 namespace {
 
 thread_local char g_err[1024];
+thread_local size_t g_err_line = 0;
 
 int fail(int code, const char* what) {
   std::snprintf(g_err, sizeof g_err, "%s", what);
@@ -62,6 +64,9 @@ int guarded(F&& f) {
     return 0;
   } catch (const SolveError& e) {
     return fail(2, e.what());
+  } catch (const ParseError& e) {
+    g_err_line = e.line();
+    return fail(4, e.what());
   } catch (const std::invalid_argument& e) {
     return fail(1, e.what());
   } catch (const std::exception& e) {
@@ -105,6 +110,7 @@ GreedyConfig greedy_config(double tol, size_t max_levels, size_t cap, int kind, 
 extern "C" {
 
 const char* ref_last_error(void) { return g_err; }
+size_t ref_last_error_line(void) { return g_err_line; }
 
 double ref_eval_wendland(int kind, double eta) { return eval_wendland(kind_of(kind), eta); }
 
@@ -415,5 +421,49 @@ extern "C" int ref_orthogonality(const double* nodes, size_t n_nodes, int dim, c
     *out_mean = q.mean_orthogonality_deg;
     *out_inverted = q.inverted_count;
     *out_degenerate = q.degenerate_count;
+  });
+}
+
+// read_su2 (mesh_io.cpp:127-259).  sizes[0..5] = dim, nodes, elements, element
+// nodes, markers, marker-name bytes (names joined by '\n'), then per-marker
+// arrays: me[m] elements, mc[m] element nodes, mn[m] nodes (caller allocates
+// after a call with xyz == nullptr).
+extern "C" int ref_read_su2(const char* path, size_t* sizes, double* xyz, int* kinds,
+                            size_t* offsets, size_t* conn, char* names, size_t* me, size_t* mc,
+                            size_t* mn, int* mkinds, size_t* moffsets, size_t* mconn,
+                            size_t* mnodes) {
+  return guarded([&] {
+    const Mesh m = read_su2(std::string(path));
+    size_t nconn = 0, nbytes = 0;
+    for (const auto& e : m.elements) nconn += e.nodes.size();
+    for (const auto& k : m.markers) nbytes += k.name.size() + 1;
+    sizes[0] = (size_t)m.dim, sizes[1] = m.nodes.size(), sizes[2] = m.elements.size();
+    sizes[3] = nconn, sizes[4] = m.markers.size(), sizes[5] = nbytes;
+    for (size_t i = 0; i < m.markers.size(); ++i) {
+      size_t c = 0;
+      for (const auto& e : m.markers[i].elements) c += e.nodes.size();
+      me[i] = m.markers[i].elements.size(), mc[i] = c, mn[i] = m.markers[i].nodes.size();
+    }
+    if (!xyz) return;
+    for (size_t i = 0; i < m.nodes.size(); ++i) put(xyz + 3 * i, m.nodes[i]);
+    offsets[0] = 0;
+    for (size_t e = 0; e < m.elements.size(); ++e) {
+      kinds[e] = static_cast<int>(m.elements[e].kind);
+      for (size_t k = 0; k < m.elements[e].nodes.size(); ++k) conn[offsets[e] + k] = m.elements[e].nodes[k];
+      offsets[e + 1] = offsets[e] + m.elements[e].nodes.size();
+    }
+    size_t pn = 0, pe = 0, pc = 0, pnod = 0;
+    for (const auto& k : m.markers) {
+      std::memcpy(names + pn, k.name.data(), k.name.size());
+      names[pn + k.name.size()] = '\n';
+      pn += k.name.size() + 1;
+      for (const auto& e : k.elements) {
+        mkinds[pe] = static_cast<int>(e.kind);
+        moffsets[pe] = e.nodes.size();
+        for (size_t v : e.nodes) mconn[pc++] = v;
+        ++pe;
+      }
+      for (size_t v : k.nodes) mnodes[pnod++] = v;
+    }
   });
 }

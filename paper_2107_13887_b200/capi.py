@@ -35,6 +35,14 @@ class SolveError(RuntimeError):
     """icemorph::SolveError (rbf.hpp:13-16)."""
 
 
+class ParseError(RuntimeError):
+    """icemorph::ParseError (mesh_io.hpp:14-21): "path:line: what"; .line."""
+
+    def __init__(self, msg: str, line: int):
+        super().__init__(msg)
+        self.line = line
+
+
 class IcemorphRuntimeError(RuntimeError):
     pass
 
@@ -98,7 +106,9 @@ EXPORTS = [
     "im_context_create", "im_context_destroy", "im_last_error", "im_last_device_ms",
     "im_version", "im_eval_wendland", "im_eval_basis", "im_make_wall_function",
     "im_eval_wall_function", "im_solve_weights", "im_eval_interpolant", "im_greedy_level",
-    "im_run_multilevel", "im_build_distance_index", "im_signed_measures", "im_count_inverted", "im_orthogonality", "im_update_volume", "im_deform",
+    "im_run_multilevel", "im_build_distance_index", "im_signed_measures", "im_count_inverted", "im_orthogonality",
+    "im_su2_read", "im_su2_write", "im_mesh_destroy", "im_mesh_sizes", "im_mesh_nodes",
+    "im_mesh_elements", "im_mesh_marker_sizes", "im_mesh_marker", "im_last_error_line", "im_update_volume", "im_deform",
     "im_volume_plan_create", "im_volume_plan_destroy", "im_volume_plan_set_controls",
     "im_volume_plan_run", "im_volume_plan_reset_field", "im_volume_plan_download_field",
     "im_volume_plan_distances", "im_volume_plan_set_level", "im_volume_plan_run_steps",
@@ -130,6 +140,18 @@ def _declare(L):
     L.im_build_distance_index.argtypes = [C.c_void_p, _pd, _sz, C.c_int, _psz, _sz, _pd]
     L.im_signed_measures.argtypes = [C.c_void_p, _pd, _sz, _pi, _psz, _psz, _sz, _pd, _psz]
     L.im_count_inverted.argtypes = [C.c_void_p, _pd, _sz, _pi, _psz, _psz, _sz, _psz]
+    L.im_su2_read.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p)]
+    L.im_mesh_destroy.argtypes = [C.c_void_p]
+    L.im_mesh_sizes.argtypes = [C.c_void_p, _pi, _psz, _psz, _psz, _psz]
+    L.im_mesh_nodes.argtypes = [C.c_void_p, _pd]
+    L.im_mesh_elements.argtypes = [C.c_void_p, _pi, _psz, _psz]
+    L.im_mesh_marker_sizes.argtypes = [C.c_void_p, _sz, _psz, _psz, _psz, _psz]
+    L.im_mesh_marker.argtypes = [C.c_void_p, _sz, C.c_char_p, _pi, _psz, _psz, _psz]
+    L.im_last_error_line.argtypes = [C.c_void_p]
+    L.im_last_error_line.restype = _sz
+    L.im_su2_write.argtypes = [C.c_void_p, C.c_char_p, C.c_int, _pd, _sz, _pi, _psz, _psz, _sz, _sz,
+                               C.POINTER(C.c_char_p), C.POINTER(_pi), C.POINTER(_psz),
+                               C.POINTER(_psz), _psz]
     L.im_orthogonality.argtypes = [C.c_void_p, _pd, _sz, _pi, _psz, _psz, _sz, _pd, _pd,
                                    C.POINTER(QualityReportC)]
     L.im_update_volume.argtypes = [C.c_void_p, _pd, _sz, _pd, _pd, _pd, _sz,
@@ -235,6 +257,8 @@ class Context:
             raise ValueError(msg)
         if rc == 2:
             raise SolveError(msg)
+        if rc == 4:
+            raise ParseError(msg, int(self.lib.im_last_error_line(self.h)))
         raise IcemorphRuntimeError(msg)
 
     @property
@@ -365,6 +389,56 @@ class Context:
             self.h, _dp(nodes), len(nodes), k.ctypes.data_as(_pi), _szp(o), _szp(c), len(k),
             C.byref(inv)))
         return int(inv.value)
+
+    def read_su2(self, path: str) -> dict:
+        """read_su2 (mesh_io.cpp:127-259): dict(dim, nodes (n, 3), elements CSR,
+        markers = [dict(name, elements CSR, nodes)])."""
+        h = C.c_void_p()
+        self._check(self.lib.im_su2_read(self.h, os.fsencode(path), C.byref(h)))
+        try:
+            L = self.lib
+            dim, nn, ne, nc, nm = C.c_int(), _sz(), _sz(), _sz(), _sz()
+            L.im_mesh_sizes(h, C.byref(dim), C.byref(nn), C.byref(ne), C.byref(nc), C.byref(nm))
+            nodes = np.zeros((nn.value, 3))
+            L.im_mesh_nodes(h, _dp(nodes))
+            k = np.zeros(ne.value, np.int32)
+            o = np.zeros(ne.value + 1, np.uint64)
+            c = np.zeros(max(nc.value, 1), np.uint64)
+            L.im_mesh_elements(h, k.ctypes.data_as(_pi), _szp(o), _szp(c))
+            markers = []
+            for m in range(nm.value):
+                ln, me, mc, mn = _sz(), _sz(), _sz(), _sz()
+                L.im_mesh_marker_sizes(h, m, C.byref(ln), C.byref(me), C.byref(mc), C.byref(mn))
+                name = C.create_string_buffer(ln.value + 1)
+                mk = np.zeros(me.value, np.int32)
+                mo = np.zeros(me.value + 1, np.uint64)
+                mcn = np.zeros(max(mc.value, 1), np.uint64)
+                mnd = np.zeros(max(mn.value, 1), np.uint64)
+                L.im_mesh_marker(h, m, name, mk.ctypes.data_as(_pi), _szp(mo), _szp(mcn), _szp(mnd))
+                markers.append(dict(name=name.value.decode(), elements=(mk, mo, mcn[:mc.value]),
+                                    nodes=mnd[:mn.value].astype(np.int64)))
+            return dict(dim=dim.value, nodes=nodes, elements=(k, o, c[:nc.value]), markers=markers)
+        finally:
+            self.lib.im_mesh_destroy(h)
+
+    def write_su2(self, path: str, dim: int, nodes, elements, markers):
+        """write_su2 (mesh_io.cpp:269-301); markers = [(name, elements CSR)]."""
+        nodes = xyz(nodes)
+        k, o, c = elements
+        k = np.ascontiguousarray(k, np.int32)
+        o = np.ascontiguousarray(o, np.uint64)
+        c = np.ascontiguousarray(c if len(c) else [0], np.uint64)
+        n = len(markers)
+        names = (C.c_char_p * max(n, 1))(*[m[0].encode() for m in markers])
+        keep = [(np.ascontiguousarray(m[1][0], np.int32), np.ascontiguousarray(m[1][1], np.uint64),
+                 np.ascontiguousarray(m[1][2] if len(m[1][2]) else [0], np.uint64)) for m in markers]
+        mk = (_pi * max(n, 1))(*[a.ctypes.data_as(_pi) for a, _, _ in keep])
+        mo = (_psz * max(n, 1))(*[_szp(b) for _, b, _ in keep])
+        mc = (_psz * max(n, 1))(*[_szp(cc) for _, _, cc in keep])
+        mn = np.array([len(a) for a, _, _ in keep] or [0], np.uint64)
+        self._check(self.lib.im_su2_write(self.h, os.fsencode(path), int(dim), _dp(nodes), len(nodes),
+                                          k.ctypes.data_as(_pi), _szp(o), _szp(c), len(k), n, names,
+                                          mk, mo, mc, _szp(mn)))
 
     def orthogonality(self, nodes, elements):
         """quality.cpp:150-236 on the device: dict(scores, measures, min, mean,

@@ -20,6 +20,7 @@
 #include "../../include/icemorph_b200.h"
 #include "greedy.hpp"
 #include "host_io.hpp"
+#include "su2_io.hpp"
 #include "runtime.hpp"
 
 namespace imb {
@@ -119,6 +120,10 @@ int guarded(im_context* ctx, F&& f) {
     f(c);
     c.status = IM_OK;
     c.message[0] = 0;
+  } catch (const ParseFailure& e) {
+    c.status = IM_PARSE_ERROR;
+    c.error_line = e.line;
+    std::snprintf(c.message, sizeof c.message, "%s", e.what());
   } catch (const InvalidArgument& e) {
     c.status = IM_INVALID_ARGUMENT;
     std::snprintf(c.message, sizeof c.message, "%s", e.what());
@@ -435,6 +440,104 @@ int im_orthogonality(im_context* ctx, const double* nodes, size_t n_nodes, const
 int im_count_inverted(im_context* ctx, const double* nodes, size_t n_nodes, const int* kinds,
                       const size_t* offsets, const size_t* conn, size_t n_elem, size_t* inverted) {
   return im_signed_measures(ctx, nodes, n_nodes, kinds, offsets, conn, n_elem, nullptr, inverted);
+}
+
+// ---- SU2 mesh I/O -------------------------------------------------------------------
+}  // extern "C"
+struct im_mesh {
+  imb::HostMesh m;
+};
+extern "C" {
+
+int im_su2_read(im_context* ctx, const char* path, im_mesh** out) {
+  if (!out) return IM_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded(ctx, [&](Context& c) {
+    auto* mesh = new im_mesh{read_su2_file(c, host_pool(c), path ? path : "")};
+    *out = mesh;
+  });
+}
+
+int im_mesh_destroy(im_mesh* mesh) {
+  delete mesh;
+  return IM_OK;
+}
+
+int im_mesh_sizes(const im_mesh* mesh, int* dim, size_t* n_nodes, size_t* n_elements,
+                  size_t* n_element_nodes, size_t* n_markers) {
+  if (!mesh) return IM_INVALID_ARGUMENT;
+  const HostMesh& m = mesh->m;
+  if (dim) *dim = m.dim;
+  if (n_nodes) *n_nodes = m.xyz.size() / 3;
+  if (n_elements) *n_elements = m.kinds.size();
+  if (n_element_nodes) *n_element_nodes = m.conn.size();
+  if (n_markers) *n_markers = m.markers.size();
+  return IM_OK;
+}
+
+int im_mesh_nodes(const im_mesh* mesh, double* xyz) {
+  if (!mesh || !xyz) return IM_INVALID_ARGUMENT;
+  std::memcpy(xyz, mesh->m.xyz.data(), mesh->m.xyz.size() * 8);
+  return IM_OK;
+}
+
+int im_mesh_elements(const im_mesh* mesh, int* kinds, size_t* offsets, size_t* nodes) {
+  if (!mesh) return IM_INVALID_ARGUMENT;
+  const HostMesh& m = mesh->m;
+  if (kinds) std::memcpy(kinds, m.kinds.data(), m.kinds.size() * sizeof(int));
+  if (offsets) std::memcpy(offsets, m.offsets.data(), m.offsets.size() * 8);
+  if (nodes) std::memcpy(nodes, m.conn.data(), m.conn.size() * 8);
+  return IM_OK;
+}
+
+int im_mesh_marker_sizes(const im_mesh* mesh, size_t marker, size_t* name_length,
+                         size_t* n_elements, size_t* n_element_nodes, size_t* n_nodes) {
+  if (!mesh || marker >= mesh->m.markers.size()) return IM_INVALID_ARGUMENT;
+  const auto& k = mesh->m.markers[marker];
+  if (name_length) *name_length = k.name.size();
+  if (n_elements) *n_elements = k.kinds.size();
+  if (n_element_nodes) *n_element_nodes = k.conn.size();
+  if (n_nodes) *n_nodes = k.nodes.size();
+  return IM_OK;
+}
+
+int im_mesh_marker(const im_mesh* mesh, size_t marker, char* name, int* kinds, size_t* offsets,
+                   size_t* element_nodes, size_t* nodes) {
+  if (!mesh || marker >= mesh->m.markers.size()) return IM_INVALID_ARGUMENT;
+  const auto& k = mesh->m.markers[marker];
+  if (name) std::memcpy(name, k.name.data(), k.name.size());
+  if (kinds) std::memcpy(kinds, k.kinds.data(), k.kinds.size() * sizeof(int));
+  if (offsets) std::memcpy(offsets, k.offsets.data(), k.offsets.size() * 8);
+  if (element_nodes) std::memcpy(element_nodes, k.conn.data(), k.conn.size() * 8);
+  if (nodes) std::memcpy(nodes, k.nodes.data(), k.nodes.size() * 8);
+  return IM_OK;
+}
+
+size_t im_last_error_line(const im_context* ctx) { return ctx ? ctx->c.error_line : 0; }
+
+int im_su2_write(im_context* ctx, const char* path, int dim, const double* xyz, size_t n_nodes,
+                 const int* kinds, const size_t* offsets, const size_t* nodes, size_t n_elements,
+                 size_t n_markers, const char* const* names, const int* const* m_kinds,
+                 const size_t* const* m_offsets, const size_t* const* m_nodes,
+                 const size_t* m_n_elements) {
+  return guarded(ctx, [&](Context& c) {
+    HostMesh m;
+    m.dim = dim;
+    m.xyz.assign(xyz, xyz + 3 * n_nodes);
+    m.kinds.assign(kinds, kinds + n_elements);
+    m.offsets.assign(offsets, offsets + n_elements + 1);
+    m.conn.assign(nodes, nodes + offsets[n_elements]);
+    for (size_t k = 0; k < n_markers; ++k) {
+      HostMesh::Marker mk;
+      mk.name = names[k];
+      const size_t ne = m_n_elements[k];
+      mk.kinds.assign(m_kinds[k], m_kinds[k] + ne);
+      mk.offsets.assign(m_offsets[k], m_offsets[k] + ne + 1);
+      mk.conn.assign(m_nodes[k], m_nodes[k] + m_offsets[k][ne]);
+      m.markers.push_back(std::move(mk));
+    }
+    write_su2_file(host_pool(c), path ? path : "", m);
+  });
 }
 
 int im_build_distance_index(im_context* ctx, const double* nodes, size_t n_nodes, int dim,

@@ -139,6 +139,8 @@ struct Chunk {
 
 }  // namespace
 
+HostPool& host_pool(Context& c) { return state(c).pool; }
+
 void staged_h2d(Context& c, const H2DJob* jobs, int n_jobs, size_t align, const ChunkScan& scan) {
   HostIOState& s = state(c);
   size_t total = 0;

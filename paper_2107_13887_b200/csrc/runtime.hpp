@@ -116,6 +116,7 @@ struct Context {
   DBuf<unsigned char> scratch;
   HBuf<unsigned char> pinned;
   double last_kernel_ms = 0.0;
+  size_t error_line = 0;  // line of the last IM_PARSE_ERROR
   // Grow-only device scratch slots reused across calls (no cudaMalloc /
   // cudaFree -- which synchronises the device -- on the hot path).
   enum Slot : int {

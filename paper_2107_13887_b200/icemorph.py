@@ -9,10 +9,10 @@ Same names, argument meaning and error behaviour as the reference binding:
 ``RuntimeError`` (``capi.SolveError``) for icemorph::SolveError, as pybind11
 maps them, plus ``orthogonality`` / ``signed_measures`` (bindings.cpp:194-197)
 and the report's ``inverted_elements`` / ``quality_before`` / ``quality_after``
-(pipeline.cpp:55, 101-102) on the device.  Mesh I/O and generators are out of
-scope; a ``Mesh`` is built from
-arrays (``Mesh(dim, nodes, markers, elements)``) instead of ``read_su2`` /
-``gen_airfoil_mesh``.
+(pipeline.cpp:55, 101-102) on the device, and ``read_su2`` / ``write_su2``
+(bindings.cpp:149-154) on the native SU2 reader / writer.  Generators are out
+of scope; a ``Mesh`` can also be built from arrays (``Mesh(dim, nodes,
+markers, elements)``).
 """
 from __future__ import annotations
 
@@ -63,11 +63,13 @@ class Mesh:
     (kind, node list) with kind an ElementKind index or name
     (``capi.ELEMENT_KINDS``), or a CSR triple from ``capi.elements_csr``."""
 
-    def __init__(self, dim: int, nodes, markers: dict, elements=()):
+    def __init__(self, dim: int, nodes, markers: dict, elements=(), marker_elements=None):
         self.dim = int(dim)
         self._nodes = capi.xyz(nodes)
         self._markers = {k: [int(i) for i in v] for k, v in markers.items()}
         self._elements = capi.elements_csr(elements)
+        # boundary elements per marker (CSR), as read_su2 returns them
+        self._marker_elements = dict(marker_elements or {})
 
     @property
     def num_nodes(self) -> int:
@@ -162,6 +164,22 @@ class DeformationReport:
         return sum(l.points for l in self.levels)
 
 
+def read_su2(path: str) -> Mesh:
+    """bindings.cpp:149-151 -> read_su2 (mesh_io.cpp:127-259): the reference's
+    grammar, validation and ParseError ("path:line: what", ``capi.ParseError``,
+    a RuntimeError with ``.line``)."""
+    d = _context().read_su2(path)
+    return Mesh(d["dim"], d["nodes"], {m["name"]: m["nodes"] for m in d["markers"]}, d["elements"],
+                {m["name"]: m["elements"] for m in d["markers"]})
+
+
+def write_su2(mesh: Mesh, path: str) -> None:
+    """bindings.cpp:152-154 -> write_su2 (mesh_io.cpp:269-301)."""
+    empty = (np.zeros(0, np.int32), np.zeros(1, np.uint64), np.zeros(0, np.uint64))
+    markers = [(name, mesh._marker_elements.get(name, empty)) for name in mesh._markers]
+    _context().write_su2(path, mesh.dim, mesh._nodes, mesh._elements, markers)
+
+
 @dataclass
 class QualityReport:
     """bindings.cpp:128-134 (quality.hpp QualityReport)."""
@@ -213,7 +231,7 @@ def deform(mesh: Mesh, displacement: DisplacementField, config: DeformationConfi
                           capi.EXACT if config.precision == "exact" else capi.FP64,
                           elements=mesh._elements,
                           compute_quality=config.compute_quality and mesh.num_elements > 0)
-    out = Mesh(mesh.dim, r["nodes"], mesh._markers, mesh._elements)
+    out = Mesh(mesh.dim, r["nodes"], mesh._markers, mesh._elements, mesh._marker_elements)
     rep = DeformationReport(marker=displacement.patch, target_max=r["target_max"],
                             surface_max_error=r["surface_max_error"],
                             surface_mean_error=r["surface_mean_error"],
