@@ -188,6 +188,18 @@ struct LevelSummary {
   double seconds = 0.0;
   ConvergenceRecord record;
 };
+// ---- mesh_io.hpp (SU2 subset) ---------------------------------------------------------
+class ParseError : public std::runtime_error {
+ public:
+  ParseError(const std::string& what, std::size_t line) : std::runtime_error(what), line_(line) {}
+  std::size_t line() const { return line_; }
+
+ private:
+  std::size_t line_ = 0;
+};
+Mesh read_su2(const std::string& path);
+void write_su2(const Mesh& mesh, const std::string& path);
+
 // ---- quality.hpp ------------------------------------------------------------------
 struct QualityReport {
   std::vector<double> element_orthogonality_deg;

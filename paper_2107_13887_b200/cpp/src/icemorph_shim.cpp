@@ -4,6 +4,7 @@
 // (eval_wendland / eval_basis / wall functions) that the reference also
 // evaluates on the host.  Every hot-path call goes to the device.
 #include <iomanip>
+#include <memory>
 #include <ostream>
 #include <unordered_set>
 
@@ -29,6 +30,7 @@ void check(int rc) {
   const std::string msg = im_last_error(ctx());
   if (rc == IM_INVALID_ARGUMENT) throw std::invalid_argument(msg);
   if (rc == IM_SOLVE_ERROR) throw SolveError(msg);
+  if (rc == IM_PARSE_ERROR) throw ParseError(msg, im_last_error_line(ctx()));
   throw std::runtime_error(msg);
 }
 
@@ -267,6 +269,65 @@ double signed_measure(const Mesh& mesh, const Element& element) {
 }
 
 std::size_t count_inverted(const Mesh& mesh) { return measures(mesh, mesh.elements, nullptr); }
+
+Mesh read_su2(const std::string& path) {
+  im_mesh* h = nullptr;
+  check(im_su2_read(ctx(), path.c_str(), &h));
+  std::unique_ptr<im_mesh, int (*)(im_mesh*)> guard(h, im_mesh_destroy);
+  int dim = 0;
+  std::size_t nn = 0, ne = 0, nc = 0, nm = 0;
+  im_mesh_sizes(h, &dim, &nn, &ne, &nc, &nm);
+  Mesh m;
+  m.dim = dim;
+  m.nodes.resize(nn);
+  if (nn) im_mesh_nodes(h, &m.nodes[0].x);
+  std::vector<int> kinds(ne);
+  std::vector<std::size_t> offsets(ne + 1), conn(nc);
+  im_mesh_elements(h, kinds.data(), offsets.data(), conn.data());
+  m.elements.resize(ne);
+  for (std::size_t e = 0; e < ne; ++e) {
+    m.elements[e].kind = static_cast<ElementKind>(kinds[e]);
+    m.elements[e].nodes.assign(conn.begin() + offsets[e], conn.begin() + offsets[e + 1]);
+  }
+  for (std::size_t k = 0; k < nm; ++k) {
+    std::size_t len = 0, me = 0, mc = 0, mn = 0;
+    im_mesh_marker_sizes(h, k, &len, &me, &mc, &mn);
+    std::string name(len, '\0');
+    std::vector<int> mk(me);
+    std::vector<std::size_t> mo(me + 1), mconn(mc);
+    Marker mark;
+    mark.nodes.resize(mn);
+    im_mesh_marker(h, k, name.data(), mk.data(), mo.data(), mconn.data(), mark.nodes.data());
+    mark.name = name;
+    mark.elements.resize(me);
+    for (std::size_t e = 0; e < me; ++e) {
+      mark.elements[e].kind = static_cast<ElementKind>(mk[e]);
+      mark.elements[e].nodes.assign(mconn.begin() + mo[e], mconn.begin() + mo[e + 1]);
+    }
+    m.markers.push_back(std::move(mark));
+  }
+  return m;
+}
+
+void write_su2(const Mesh& mesh, const std::string& path) {
+  const ElementCsr csr(mesh.elements);
+  std::vector<ElementCsr> mcsr;
+  for (const auto& k : mesh.markers) mcsr.emplace_back(k.elements);
+  std::vector<const char*> names;
+  std::vector<const int*> mk;
+  std::vector<const std::size_t*> mo, mc;
+  std::vector<std::size_t> mn;
+  for (std::size_t k = 0; k < mesh.markers.size(); ++k) {
+    names.push_back(mesh.markers[k].name.c_str());
+    mk.push_back(mcsr[k].kinds.data());
+    mo.push_back(mcsr[k].offsets.data());
+    mc.push_back(mcsr[k].conn());
+    mn.push_back(mesh.markers[k].elements.size());
+  }
+  check(im_su2_write(ctx(), path.c_str(), mesh.dim, xyz(mesh.nodes), mesh.nodes.size(),
+                     csr.kinds.data(), csr.offsets.data(), csr.conn(), mesh.elements.size(),
+                     mesh.markers.size(), names.data(), mk.data(), mo.data(), mc.data(), mn.data()));
+}
 
 QualityReport orthogonality(const Mesh& mesh) {
   const ElementCsr csr(mesh.elements);

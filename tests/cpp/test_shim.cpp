@@ -130,6 +130,29 @@ int main() {
   const QualityReport q = orthogonality(tris);
   CHECK(std::abs(q.element_orthogonality_deg[0] - 90.0) < 1e-10 &&
         std::abs(q.element_orthogonality_deg[1] - 90.0) < 1e-10 && q.inverted_count == 0);
+  // mesh_io: write the triangle pair, read it back (test_mesh_io.cpp:103-124)
+  {
+    Mesh sq = tris;
+    Marker wall;
+    wall.name = "wall";
+    wall.elements = {{ElementKind::Line, {0, 1}}, {ElementKind::Line, {1, 2}}};
+    sq.markers = {wall};
+    const std::string path = "/tmp/imb_shim_square.su2";
+    write_su2(sq, path);
+    const Mesh back = read_su2(path);
+    CHECK(back.nodes.size() == 4 && back.nodes[2] == sq.nodes[2] && back.elements.size() == 2);
+    CHECK(back.markers.size() == 1 && back.markers[0].nodes == std::vector<std::size_t>({0, 1, 2}));
+    std::FILE* f = std::fopen(path.c_str(), "a");
+    std::fputs("BOGUS= 1\n", f);
+    std::fclose(f);
+    bool parse_error = false;
+    try {
+      read_su2(path);
+    } catch (const ParseError& e) {
+      parse_error = e.line() > 0 && std::string(e.what()).find("unknown section") != std::string::npos;
+    }
+    CHECK(parse_error);
+  }
   std::printf(failures ? "shim: %d FAILED\n" : "shim: all passed\n", failures);
   return failures ? 1 : 0;
 }
