@@ -31,6 +31,7 @@
 // reference.  L is stored column-major packed (column i = rows i..cap-1
 // contiguous) because both the append and the backward chain walk columns.
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <string>
@@ -251,7 +252,7 @@ __device__ __forceinline__ void bw_arrive(uint64_t* bar) {
 
 constexpr int kBwPad = kBwBlock + 32;
 
-template <bool XS_SMEM>
+template <bool XS_SMEM, bool TAIL>
 __global__ void __launch_bounds__(64) k_backward_t(GView g) {
   const GState& st = *g.st;
   if (st.status != 0) return;
@@ -339,14 +340,17 @@ __global__ void __launch_bounds__(64) k_backward_t(GView g) {
     double* cx = comp + (size_t)lane * cap;
     cx[n - 1] = exact::div_rcp(cx[n - 1], exact::make_recip(dd[n - 1]));  // x_{n-1}
     BwBlock cur{n - 2, 0};
-    double s = 0.0;
+    double s = 0.0, rcp_i = 0.0;
     for (int t = 0; cur.i >= 0; ++t) {
       const int pb = t & 1, i = cur.i;
       int off, cnt;
       src_of(cur, off, cnt);
       bw_wait(&full[pb], (uint32_t)((t >> 1) & 1));
       const double* pa = P + pb * 3 * kBwPad + lane * kBwPad;
-      if (cur.e0 == 0) s = exact::sub(cx[i], exact::mul(headL[pb], cx[i + 1]));
+      if (cur.e0 == 0) {
+        s = exact::sub(cx[i], exact::mul(headL[pb], cx[i + 1]));
+        if (TAIL) rcp_i = g.diag[i].y;
+      }
       // ping-pong register sets: loads of one 16-group run under the chain of
       // the other (no rotation moves); pa is padded so whole groups are safe.
       double ra[16], rb[16];
@@ -363,9 +367,37 @@ __global__ void __launch_bounds__(64) k_backward_t(GView g) {
 #pragma unroll
         for (int u = 0; u < 16; ++u) s = exact::sub(s, rb[u]);
       }
-      for (; e < cnt; ++e) s = exact::sub(s, pa[e]);
+      if (TAIL) {
+        // the last 0..31 elements: ra already holds pa[e..e+15] (prefetched by
+        // the loop), rb is loaded up front; sub-groups of 4 padded with +0
+        // (s - (+0) == s bit for bit, also for s = -0), so no per-element
+        // load -> subtract round trips on the chain
+        const int rem = cnt - e;
+        if (rem > 16) {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) rb[u] = pa[e + 16 + u];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (4 * q < rem) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) s = exact::sub(s, 4 * q + v < rem ? ra[4 * q + v] : 0.0);
+          }
+        if (rem > 16) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (16 + 4 * q < rem) {
+#pragma unroll
+              for (int v = 0; v < 4; ++v)
+                s = exact::sub(s, 16 + 4 * q + v < rem ? rb[4 * q + v] : 0.0);
+            }
+        }
+      } else {
+        for (; e < cnt; ++e) s = exact::sub(s, pa[e]);
+      }
       const BwBlock nx = next(cur);
-      if (nx.i != i) cx[i] = exact::div_rcp(s, exact::make_recip(dd[i]));  // x_i = s / L_ii
+      if (nx.i != i)  // x_i = s / L_ii, reciprocal of L_ii from k_insert (prefetched)
+        cx[i] = exact::div_rcp(s, TAIL ? exact::Recip{dd[i], rcp_i} : exact::make_recip(dd[i]));
       __syncwarp(0x7u);
       if (lane == 0) bw_arrive(&empty[pb]);
       cur = nx;
@@ -519,10 +551,10 @@ GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap
     xs_.reserve((size_t)cap * 4);
     bw_smem_ = head;
   }
-  IMB_CHECK(cudaFuncSetAttribute(k_backward_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(bw_smem_, 48 * 1024)));
-  IMB_CHECK(cudaFuncSetAttribute(k_backward_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(bw_smem_, 48 * 1024)));
+  for (auto k : {k_backward_t<true, true>, k_backward_t<false, true>, k_backward_t<true, false>,
+                 k_backward_t<false, false>})
+    IMB_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::max<size_t>(bw_smem_, 48 * 1024)));
   // k_insert: rr + ring[2] (+ dg staging, which also makes room for y)
   ins_smem_ = (size_t)cap * 24;
   if ((size_t)cap * 40 + 16 <= 210 * 1024) ins_smem_ = (size_t)cap * 40 + 16, ins_dg_smem_ = 1;
@@ -592,10 +624,17 @@ const GState& GreedyEngine::poll() {
 }
 
 void GreedyEngine::launch_backward(const GView& g) {
-  if (xs_.p)
-    k_backward_t<false><<<1, 64, bw_smem_, ctx_.stream>>>(g);
-  else
-    k_backward_t<true><<<1, 64, bw_smem_, ctx_.stream>>>(g);
+  const bool tail = !std::getenv("IMB_BW_OLD_TAIL");  // A/B of the row-tail schedule
+  if (tail) {
+    if (xs_.p)
+      k_backward_t<false, true><<<1, 64, bw_smem_, ctx_.stream>>>(g);
+    else
+      k_backward_t<true, true><<<1, 64, bw_smem_, ctx_.stream>>>(g);
+  } else if (xs_.p) {
+    k_backward_t<false, false><<<1, 64, bw_smem_, ctx_.stream>>>(g);
+  } else {
+    k_backward_t<true, false><<<1, 64, bw_smem_, ctx_.stream>>>(g);
+  }
 }
 
 void GreedyEngine::enqueue_step(bool sweep) {
