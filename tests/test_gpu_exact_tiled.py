@@ -7,6 +7,7 @@ farther than R and replaces the branches of sqrt / division / the eta >= 1
 cut by range-guarded branch-free forms; every case here must still equal the
 reference exactly (np.array_equal on the values)."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -151,3 +152,22 @@ def test_volume_plan_single_level_run(gpu, oracle):
             assert np.array_equal(f, v0)
         else:
             assert np.abs(f - v0).max() <= 1e-10 * np.abs(v0).max()
+
+
+def test_cfg2_levels_slice_matches_reference(gpu, oracle):
+    """Full BASELINE cfg2 geometry and the device greedy's own levels 0-1
+    (166 / 1425 controls; bit-identical to the reference's selection,
+    test_cfg2_full_selection): the exact volume update on 40k mesh nodes
+    closest to the wall equals the reference's update_volume bit for bit."""
+    w = W.cfg2()
+    pos = w.nodes[w.surface]
+    m = gpu.run_multilevel(pos, w.displacement, w.tol, 2, w.cap, w.kind, w.R)
+    d = gpu.build_distance_index(w.nodes, 2, w.surface)
+    pick = np.sort(np.argsort(d)[:40000])
+    nodes, dd = np.ascontiguousarray(w.nodes[pick]), np.ascontiguousarray(d[pick])
+    for lv in m.levels:
+        c = pos[lv.control_indices]
+        i0, v0 = oracle.update_volume(nodes, dd, c, lv.alpha, w.D, w.psi_kind, "c2", w.R,
+                                      nthreads=os.cpu_count() or 1)
+        i1, v1 = gpu.update_volume(nodes, dd, c, lv.alpha, w.D, w.psi_kind, "c2", w.R, capi.EXACT)
+        assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
