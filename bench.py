@@ -243,14 +243,21 @@ def run_b200(args):
                 else (16 if dim == 3 else 14)}
 
     # --- e2e through the public C-ABI with host buffers ----------------------
+    # inputs and outputs in page-locked host memory (the e2e contract): the
+    # library DMAs them directly; H2D of nodes / distances / controls and D2H
+    # of the sparse update stay inside the timed region every step
     d_host = plan.distances()
+    pin = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()
+    nodes_p, d_p = pin(nodes.shape, torch.float64), pin(d_host.shape, torch.float64)
+    nodes_p[:], d_p[:] = nodes, d_host
+    out_p = (pin((len(nodes),), torch.int64).view(np.uint64), pin((len(nodes), 3), torch.float64))
     e2e_times, h2d, d2h = [], 0, 0
     for it in range(max(1, min(args.steps, 5)) + 1):
         t0 = time.perf_counter()
         h2d = d2h = 0
         for c, a in levels:
-            idx, val = ctx.update_volume(nodes, d_host, c, a, D, wl["psi_kind"], "c2", R,
-                                         prec)
+            idx, val = ctx.update_volume(nodes_p, d_p, c, a, D, wl["psi_kind"], "c2", R, prec,
+                                         out=out_p)
             h2d += nodes.nbytes + d_host.nbytes + c.nbytes + a.nbytes
             d2h += idx.size * 4 + val.nbytes
         if it:  # first pass is warm-up
@@ -262,7 +269,8 @@ def run_b200(args):
         e2e_s = float(t.item())
     e2e = {"value": round(world * pairs_step / e2e_s / 1e9, 3), "unit": UNIT,
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-           "api": "im_update_volume (update_volume, wall_distance.hpp:40-42) per level"}
+           "api": "im_update_volume (update_volume, wall_distance.hpp:40-42) per level",
+           "host_buffers": "page-locked inputs and outputs"}
 
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,

@@ -352,14 +352,22 @@ class Context:
         return out
 
     def update_volume(self, nodes, dist, ctrl, alpha, D, psi_kind=0, kind="c2", R=1.0,
-                      precision=FP64):
+                      precision=FP64, out=None):
+        """update_volume (wall_distance.cpp:46-64): (node ids, values).  ``out``
+        = (uint64 ids[n], float64 values[n, 3]) reuses caller buffers (e.g.
+        page-locked ones, which the library then fills by direct DMA)."""
         nodes, c, a = xyz(nodes), xyz(ctrl), xyz(alpha)
         dist = np.ascontiguousarray(dist, dtype=np.float64)
         if len(dist) != len(nodes):
             raise ValueError("distance index does not match the mesh")
         n = len(nodes)
-        idx = np.empty(max(n, 1), np.uint64)
-        val = np.empty((max(n, 1), 3))
+        if out is None:
+            idx = np.empty(max(n, 1), np.uint64)
+            val = np.empty((max(n, 1), 3))
+        else:
+            idx, val = out
+            if len(idx) < n or len(val) < n or idx.dtype != np.uint64 or val.dtype != np.float64:
+                raise ValueError("out buffers too small or of the wrong type")
         cnt = _sz()
         wf = WallFunctionC(1.0, D, psi_kind)
         self._check(self.lib.im_update_volume(self.h, _dp(nodes), n, _dp(dist), _dp(c), _dp(a),

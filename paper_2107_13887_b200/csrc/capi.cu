@@ -579,19 +579,10 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     uint32_t* active = c.buf<uint32_t>(Context::kSlotActive, n_nodes);
     double* stage = c.buf<double>(Context::kSlotStage, 3 * n_nodes + 6 * nc);
     const bool exact = precision == IM_EXACT;
-    // nodes + distances through the pinned staging pool; the staging pass
-    // also checks for planar input (z == 0 everywhere -> the 2-D kernel)
-    std::atomic<bool> nonplanar{false};
+    // nodes + distances through the pinned staging pool (or straight to the
+    // copy engine when the caller's arrays are page-locked)
     const H2DJob up[2] = {{stage, nodes, n_nodes * 24}, {dd, dist, n_nodes * 8}};
-    staged_h2d(c, up, 2, 192, [&](int job, const unsigned char* p, size_t, size_t len) {
-      if (job != 0 || nonplanar.load(std::memory_order_relaxed)) return;
-      const double* v = reinterpret_cast<const double*>(p);
-      for (size_t i = 2; i < len / 8; i += 3)
-        if (v[i] != 0.0) {
-          nonplanar.store(true, std::memory_order_relaxed);
-          return;
-        }
-    });
+    staged_h2d(c, up, 2);
     aos_to_soa(c, stage, n_nodes, dx, dy, dz);
     tr.mark("h2d nodes+dist");
     double* tiles = c.buf<double>(Context::kSlotTiles, ctrl_tile_doubles(nc));
@@ -609,10 +600,14 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     }
     // exact: the tiled kernel (spatial order + exact-safe culling) when the
     // coordinate / R ranges allow its branch-free sqrt and division
+    // planar input (z == 0 everywhere) runs the 2-D kernels; the range of the
+    // coordinates decides the exact path's kernel (one device reduction)
+    double max_z = 0.0;
+    const double max_abs = max_abs_points(c, dx, dy, dz, n_nodes, &max_z);
     bool tiled_exact = false;
     double *midx = nullptr, *mbox = nullptr;
     if (exact) {
-      double m = max_abs_points(c, dx, dy, dz, n_nodes);
+      double m = max_abs;
       for (size_t i = 0; i < 3 * nc; ++i) m = std::max(m, std::fabs(ctrl[i]));
       tiled_exact = exact_tiled_ok(basis.support_radius, m);
       if (tiled_exact) {
@@ -623,7 +618,7 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
         pack_exact_index_host(c, ctrl, nc, 1.0 / basis.support_radius, midx, mbox);
       }
     }
-    bool planar = !nonplanar.load();
+    bool planar = max_z == 0.0;
     for (size_t i = 0; i < nc && planar; ++i) planar = ctrl[3 * i + 2] == 0.0 && alpha[3 * i + 2] == 0.0;
     tr.mark("controls + planar");
     EventTimer tm(c.stream);

@@ -100,6 +100,17 @@ namespace {
 constexpr size_t kChunk = 1u << 20;
 constexpr int kMaxEvents = 128;
 
+// page-locked (cudaHostAlloc / cudaHostRegister) host memory: the DMA engine
+// reads / writes it directly, no staging pass
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free error of a pageable pointer query
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 HostIOState& state(Context& c) {
   if (!c.io) {
     const unsigned hw = std::thread::hardware_concurrency();
@@ -143,6 +154,36 @@ HostPool& host_pool(Context& c) { return state(c).pool; }
 
 void staged_h2d(Context& c, const H2DJob* jobs, int n_jobs, size_t align, const ChunkScan& scan) {
   HostIOState& s = state(c);
+  // caller-pinned sources go straight to the copy engine (the optional scan
+  // then reads the source in parallel, overlapping the DMA)
+  std::vector<H2DJob> staged;
+  std::vector<int> staged_id;
+  for (int j = 0; j < n_jobs; ++j) {
+    if (jobs[j].bytes && is_pinned(jobs[j].src)) {
+      IMB_CHECK(cudaMemcpyAsync(jobs[j].dst, jobs[j].src, jobs[j].bytes, cudaMemcpyHostToDevice,
+                                c.stream));
+      if (scan) {
+        const size_t step = std::max(align, kChunk / align * align);
+        const int nch = (int)((jobs[j].bytes + step - 1) / step);
+        s.pool.run(nch, [&](int i) {
+          const size_t off = (size_t)i * step;
+          scan(j, static_cast<const unsigned char*>(jobs[j].src) + off, off,
+               std::min(step, jobs[j].bytes - off));
+        });
+      }
+    } else {
+      staged.push_back(jobs[j]);
+      staged_id.push_back(j);
+    }
+  }
+  if (staged.size() != (size_t)n_jobs) {
+    if (staged.empty()) return;
+    // remaining pageable jobs: recurse with the original job ids for the scan
+    const ChunkScan remap = scan ? ChunkScan([&](int k, const unsigned char* p, size_t off, size_t len) {
+      scan(staged_id[k], p, off, len);
+    }) : ChunkScan();
+    return staged_h2d(c, staged.data(), (int)staged.size(), align, remap);
+  }
   size_t total = 0;
   for (int j = 0; j < n_jobs; ++j) total += (jobs[j].bytes + 15) & ~size_t(15);
   if (total == 0) return;
@@ -192,48 +233,64 @@ void staged_h2d(Context& c, const H2DJob* jobs, int n_jobs, size_t align, const 
   }
 }
 
-void staged_d2h(Context& c, const D2HJob* jobs, int n_jobs) {
+void staged_d2h(Context& c, const D2HJob* all_jobs, int n_all) {
   HostIOState& s = state(c);
+  // caller-pinned destinations of plain copies get one direct DMA each; the
+  // rest is chunked through pinned staging.  Order: staged chunk DMAs first
+  // (their host copy-out then overlaps the direct DMAs), then direct ones.
+  std::vector<D2HJob> jobs, direct;
+  for (int j = 0; j < n_all; ++j) {
+    if (!all_jobs[j].widen_u32 && all_jobs[j].count && is_pinned(all_jobs[j].dst))
+      direct.push_back(all_jobs[j]);
+    else
+      jobs.push_back(all_jobs[j]);
+  }
+  const int n_jobs = (int)jobs.size();
   size_t total = 0;
   for (int j = 0; j < n_jobs; ++j) total += (jobs[j].count * jobs[j].src_size + 15) & ~size_t(15);
-  if (total == 0) return;
-  unsigned char* pin = s.pin_out.reserve(total);
-  const size_t target = std::max(kChunk, (total + kMaxEvents - 1) / kMaxEvents);
   std::vector<Chunk> chunks;
-  size_t stage = 0;
-  for (int j = 0; j < n_jobs; ++j) {
-    const size_t per = std::max<size_t>(1, target / jobs[j].src_size);
-    for (size_t off = 0; off < jobs[j].count; off += per)
-      chunks.push_back({j, off, std::min(per, jobs[j].count - off),
-                        stage + off * jobs[j].src_size});
-    stage += (jobs[j].count * jobs[j].src_size + 15) & ~size_t(15);
-  }
-  while (s.ev.size() < chunks.size()) {
-    cudaEvent_t e;
-    IMB_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    s.ev.push_back(e);
-  }
-  for (size_t i = 0; i < chunks.size(); ++i) {
-    const Chunk& k = chunks[i];
-    const D2HJob& jb = jobs[k.job];
-    IMB_CHECK(cudaMemcpyAsync(pin + k.stage,
-                              static_cast<const unsigned char*>(jb.src) + k.off * jb.src_size,
-                              k.len * jb.src_size, cudaMemcpyDeviceToHost, c.stream));
-    IMB_CHECK(cudaEventRecord(s.ev[i], c.stream));
-  }
-  s.pool.run((int)chunks.size(), [&](int i) {
-    const Chunk& k = chunks[i];
-    const D2HJob& jb = jobs[k.job];
-    IMB_CHECK(cudaEventSynchronize(s.ev[i]));
-    if (jb.widen_u32) {
-      const uint32_t* src = reinterpret_cast<const uint32_t*>(pin + k.stage);
-      uint64_t* dst = static_cast<uint64_t*>(jb.dst) + k.off;
-      for (size_t e = 0; e < k.len; ++e) dst[e] = src[e];
-    } else {
-      std::memcpy(static_cast<unsigned char*>(jb.dst) + k.off * jb.src_size, pin + k.stage,
-                  k.len * jb.src_size);
+  unsigned char* pin = nullptr;
+  if (total) {
+    pin = s.pin_out.reserve(total);
+    const size_t target = std::max(kChunk, (total + kMaxEvents - 1) / kMaxEvents);
+    size_t stage = 0;
+    for (int j = 0; j < n_jobs; ++j) {
+      const size_t per = std::max<size_t>(1, target / jobs[j].src_size);
+      for (size_t off = 0; off < jobs[j].count; off += per)
+        chunks.push_back({j, off, std::min(per, jobs[j].count - off), stage + off * jobs[j].src_size});
+      stage += (jobs[j].count * jobs[j].src_size + 15) & ~size_t(15);
     }
-  });
+    while (s.ev.size() < chunks.size()) {
+      cudaEvent_t e;
+      IMB_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      s.ev.push_back(e);
+    }
+    for (size_t i = 0; i < chunks.size(); ++i) {
+      const Chunk& k = chunks[i];
+      const D2HJob& jb = jobs[k.job];
+      IMB_CHECK(cudaMemcpyAsync(pin + k.stage,
+                                static_cast<const unsigned char*>(jb.src) + k.off * jb.src_size,
+                                k.len * jb.src_size, cudaMemcpyDeviceToHost, c.stream));
+      IMB_CHECK(cudaEventRecord(s.ev[i], c.stream));
+    }
+  }
+  for (const D2HJob& jb : direct)
+    IMB_CHECK(cudaMemcpyAsync(jb.dst, jb.src, jb.count * jb.src_size, cudaMemcpyDeviceToHost, c.stream));
+  if (!chunks.empty())
+    s.pool.run((int)chunks.size(), [&](int i) {
+      const Chunk& k = chunks[i];
+      const D2HJob& jb = jobs[k.job];
+      IMB_CHECK(cudaEventSynchronize(s.ev[i]));
+      if (jb.widen_u32) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(pin + k.stage);
+        uint64_t* dst = static_cast<uint64_t*>(jb.dst) + k.off;
+        for (size_t e = 0; e < k.len; ++e) dst[e] = src[e];
+      } else {
+        std::memcpy(static_cast<unsigned char*>(jb.dst) + k.off * jb.src_size, pin + k.stage,
+                    k.len * jb.src_size);
+      }
+    });
+  if (!direct.empty()) IMB_CHECK(cudaStreamSynchronize(c.stream));
 }
 
 }  // namespace imb

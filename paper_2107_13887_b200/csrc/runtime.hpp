@@ -203,8 +203,10 @@ struct VolumeArgs {
 };
 
 void launch_volume(Context& ctx, const VolumeArgs& a);
-// max |coordinate| over device SoA points (synchronous, 8-byte readback)
-double max_abs_points(Context& ctx, const double* x, const double* y, const double* z, size_t n);
+// max |coordinate| over device SoA points (synchronous, 16-byte readback);
+// *max_abs_z (optional) = max |z| (0 <=> planar input)
+double max_abs_points(Context& ctx, const double* x, const double* y, const double* z, size_t n,
+                      double* max_abs_z = nullptr);
 // ranges under which the tiled exact kernel's sqrt/division shortcuts are
 // bit-exact: |coordinates| <= 1e100, R in [1e-100, 1e100]
 inline bool exact_tiled_ok(double R, double max_abs) {

@@ -171,3 +171,26 @@ def test_cfg2_levels_slice_matches_reference(gpu, oracle):
                                       nthreads=os.cpu_count() or 1)
         i1, v1 = gpu.update_volume(nodes, dd, c, lv.alpha, w.D, w.psi_kind, "c2", w.R, capi.EXACT)
         assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
+
+
+def test_update_volume_pinned_buffers(gpu):
+    """Page-locked inputs / outputs take the direct-DMA path of the host
+    transfers (host_io.cu); results equal the staged (pageable) path."""
+    import torch
+
+    rng = np.random.default_rng(12)
+    nodes, ctrl = rng.random((50000, 3)), rng.random((900, 3))
+    alpha, d = rng.standard_normal((900, 3)), rng.random(50000)
+    i0, v0 = gpu.update_volume(nodes, d, ctrl, alpha, 0.7, 0, "c2", 0.2, capi.EXACT)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    out = (torch.empty(50000, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64),
+           torch.empty((50000, 3), dtype=torch.float64, pin_memory=True).numpy())
+    i1, v1 = gpu.update_volume(pin(nodes), pin(d), ctrl, alpha, 0.7, 0, "c2", 0.2, capi.EXACT, out=out)
+    assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
+    planar = nodes.copy()
+    planar[:, 2] = 0.0
+    c2, a2 = ctrl.copy(), alpha.copy()
+    c2[:, 2] = a2[:, 2] = 0.0
+    i2, v2 = gpu.update_volume(planar, d, c2, a2, 0.7, 0, "c2", 0.2, capi.FP64)
+    i3, v3 = gpu.update_volume(pin(planar), pin(d), c2, a2, 0.7, 0, "c2", 0.2, capi.FP64, out=out)
+    assert np.array_equal(i2, i3) and np.array_equal(v2, v3)  # planar detection on the direct path

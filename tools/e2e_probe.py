@@ -65,11 +65,19 @@ def main():
     for _ in range(5):
         np.zeros((len(nodes), 3))[:] = 1.0
     print(f"np.zeros+touch 24MB: {(time.perf_counter() - t) / 5 * 1e3:.2f} ms", file=sys.stderr)
+    pinned = os.environ.get("PROBE_PINNED") == "1"
+    prec = capi.EXACT if os.environ.get("PROBE_EXACT") == "1" else capi.FP64
+    out = None
+    if pinned:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        nodes, d = pin(nodes), pin(d)
+        out = (torch.empty(len(nodes), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64),
+               torch.empty((len(nodes), 3), dtype=torch.float64, pin_memory=True).numpy())
     for it in range(3):
         t0 = time.perf_counter()
         for c, a in levels:
             t = time.perf_counter()
-            idx, val = ctx.update_volume(nodes, d, c, a, w.D, 0, "c2", w.R, capi.FP64)
+            idx, val = ctx.update_volume(nodes, d, c, a, w.D, 0, "c2", w.R, prec, out=out)
             print(f"  level nc={len(c)}: {(time.perf_counter() - t) * 1e3:.2f} ms "
                   f"(kernel {ctx.last_device_ms:.2f} ms, {len(idx)} entries)", file=sys.stderr)
         print(f"step {it}: {(time.perf_counter() - t0) * 1e3:.2f} ms", file=sys.stderr)
