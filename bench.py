@@ -59,6 +59,9 @@ FLOPS = {2: (17.0, 7.0), 3: (22.0, 10.0)}
 # (tools/fp64_probe.cu: 34.2 TFLOP/s at 8 CTAs/SM); MEASURED_PEAKS.json has
 # no FP64 entry.  Nominal 148 SM x 64 DFMA x 2 x 1.965 GHz = 37.2 TFLOP/s.
 FP64_PEAK_TFLOPS = 34.2
+# FP32 (FFMA / packed FFMA2) peak measured with tools/f32_probe.cu on the same
+# pool; nominal 148 SM x 128 lanes x 2 x 1.965 GHz = 74.4 TFLOP/s.
+FP32_PEAK_TFLOPS = 74.4
 
 
 def peaks():
@@ -163,7 +166,8 @@ def run_b200(args):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = capi.Context(local)
-    prec = capi.EXACT if args.precision == "exact" else capi.FP64
+    prec = {"exact": capi.EXACT, "fp64": capi.FP64, "fp32": capi.FP32}[args.precision]
+    peak = FP32_PEAK_TFLOPS if prec == capi.FP32 else FP64_PEAK_TFLOPS
     wl = build_workload(args.workload, args.scale)
     nodes, surface, dim = wl["nodes"], wl["surface"], wl["dim"]
     R, D = wl["R"], wl["D"]
@@ -231,16 +235,19 @@ def run_b200(args):
     useful_launch = fin * in_step / launches_per_step
     achieved_tf = useful_launch / (kern_ms * 1e-3) / 1e12
     dense_tf = flops_step / launches_per_step / (kern_ms * 1e-3) / 1e12
-    roofline = {"bound": "fp64", "achieved": round(achieved_tf, 3),
-                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": round(achieved_tf / FP64_PEAK_TFLOPS, 4), "traffic": None,
-                "peak_source": "measured DFMA microbenchmark (tools/fp64_probe.cu)",
+    roofline = {"bound": "fp32" if prec == capi.FP32 else "fp64", "achieved": round(achieved_tf, 3),
+                "peak": peak, "unit": "TFLOP/s",
+                "frac": round(achieved_tf / peak, 4), "traffic": None,
+                "peak_source": "nominal FP32 (148 SM x 128 lanes x 2 x 1.965 GHz)"
+                if prec == capi.FP32 else "measured DFMA microbenchmark (tools/fp64_probe.cu)",
                 "useful_flops_per_launch": useful_launch,
                 "flops_per_pair_in_support": fin,
                 "in_support_fraction": round(in_step / max(pairs_step, 1), 4),
                 "dense_equivalent_tflops": round(dense_tf, 3),
                 "fp64_instructions_per_pair": (30 if dim == 3 else 25) if prec == capi.EXACT
-                else (16 if dim == 3 else 14)}
+                else 0 if prec == capi.FP32 else (16 if dim == 3 else 14)}
+    if prec == capi.FP32:
+        roofline["fp32_lane_ops_per_pair"] = 13 if dim == 3 else 10
 
     # --- e2e through the public C-ABI with host buffers ----------------------
     # inputs and outputs in page-locked host memory (the e2e contract): the
@@ -275,7 +282,8 @@ def run_b200(args):
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 pairs, f64 sums" if prec == capi.FP32 else "f64",
         "data": "synthetic (seeded generator, paper_2107_13887_b200/workloads.py)",
         "config": {"workload": wl["name"], "n_nodes": int(len(nodes)),
                    "n_surface": int(len(surface)), "n_controls_per_level": n_ctrl,
@@ -294,6 +302,9 @@ def run_b200(args):
     if prec == capi.EXACT and not args.no_fast:
         out["fp64_fast"] = fast_section(args, plan, levels, wl, R, D, pairs_step, fin, in_step,
                                         launches_per_step, world, capi)
+        if wl["fixed_controls"] is not None:  # FP32 mode: well-conditioned weights only
+            out["fp32"] = fast_section(args, plan, levels, wl, R, D, pairs_step, fin, in_step,
+                                       launches_per_step, world, capi, capi.FP32)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, levels, d_host, budget_s=args.cpu_seconds)
     if rank == 0:
@@ -303,23 +314,29 @@ def run_b200(args):
 
 
 def fast_section(args, plan, levels, wl, R, D, pairs_step, fin, in_step, launches_per_step, world,
-                 capi):
+                 capi, prec=None):
     """The FP64 fast path (FMA-contracted, Morton-ordered controls, rsqrt-based
     distances) on the same resident plan: throughput, roofline fraction and
     its measured deviation from the exact (reference-identical) field after
     one step.  The deviation is bounded below by the conditioning of the
     reference's weights (sum|alpha| / max|dV| reaches 1e7-1e11 on these
-    configs), which is why the headline uses the exact mode."""
+    configs), which is why the headline uses the exact mode.  With prec=FP32:
+    the FP32 evaluation mode (packed FP32 pair arithmetic, 1e-5 bar), reported
+    against the FP32 peak; only for well-conditioned weights (raw sweep)."""
+    prec = capi.FP64 if prec is None else prec
+    for l, (c, a) in enumerate(levels):
+        plan.set_level(l, c, a, D, wl["psi_kind"], "c2", R, capi.EXACT)
     plan.reset_field()
     plan.run_steps(1, "c2", R, capi.EXACT, flush_l2=False)
     f_exact = plan.field()
     for l, (c, a) in enumerate(levels):
-        plan.set_level(l, c, a, D, wl["psi_kind"], "c2", R, capi.FP64)
+        plan.set_level(l, c, a, D, wl["psi_kind"], "c2", R, prec)
     plan.reset_field()
-    plan.run_steps(1, "c2", R, capi.FP64, flush_l2=False)
+    plan.run_steps(1, "c2", R, prec, flush_l2=False)
     f_fast = plan.field()
-    plan.run_steps(args.warmup, "c2", R, capi.FP64, flush_l2=True)
-    st = plan.run_steps(args.steps, "c2", R, capi.FP64, flush_l2=True)
+    plan.run_steps(args.warmup, "c2", R, prec, flush_l2=True)
+    st = plan.run_steps(args.steps, "c2", R, prec, flush_l2=True)
+    peak = FP32_PEAK_TFLOPS if prec == capi.FP32 else FP64_PEAK_TFLOPS
     step_ms = st["step_ms_total"] / args.steps
     kern_ms = st["kernel_ms_total"] / max(st["kernel_launches"], 1)
     tf = fin * in_step / launches_per_step / (kern_ms * 1e-3) / 1e12
@@ -329,11 +346,14 @@ def fast_section(args, plan, levels, wl, R, D, pairs_step, fin, in_step, launche
     smax = float(np.sqrt((disp ** 2).sum(axis=1)).max()) if disp is not None else None
     return {"value": round(world * pairs_step / (step_ms * 1e-3) / 1e9, 3), "unit": UNIT,
             "ms_per_step": round(step_ms, 4), "kernel_ms_avg": round(kern_ms, 4),
-            "roofline_frac": round(tf / FP64_PEAK_TFLOPS, 4), "achieved_tflops": round(tf, 3),
+            "roofline_frac": round(tf / peak, 4), "achieved_tflops": round(tf, 3),
+            "roofline_peak_tflops": peak,
             "max_abs_dev_vs_exact": dev,
             "rel_dev_vs_max_field": dev / scale if scale else None,
             "rel_dev_vs_max_surface_disp": dev / smax if smax else None,
-            "note": "FMA fast path; agreement limited by the reference weights' conditioning"}
+            "note": "FP32 pair arithmetic (FFMA2), FP64 per-tile sums; bar 1e-5 of max field"
+            if prec == capi.FP32 else
+            "FMA fast path; agreement limited by the reference weights' conditioning"}
 
 
 def cpu_baseline(wl, levels, dist, budget_s=12.0, nthreads=None):
@@ -442,9 +462,9 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--precision", default="exact", choices=["fp64", "exact"],
+    ap.add_argument("--precision", default="exact", choices=["fp64", "exact", "fp32"],
                     help="volume-update arithmetic of the headline: exact (bit-identical to the "
-                         "reference, default) or fp64 (FMA fast path)")
+                         "reference, default), fp64 (FMA fast path) or fp32 (FP32 mode)")
     ap.add_argument("--no-fast", action="store_true",
                     help="skip the secondary FP64 fast-path measurement")
     ap.add_argument("--greedy-cache", default=None, help="development: save/load the control sets")

@@ -23,6 +23,11 @@
  *   IM_EXACT   reference arithmetic order, bit-identical results
  *   IM_FP64    FMA fast path, <= 1e-10 relative to the reference (default
  *              for the volume update)
+ *   IM_FP32    the pair arithmetic in FP32 (packed FFMA2, two controls per
+ *              instruction) with FP64 coordinates, per-tile FP64 sums and
+ *              FP64 outputs: <= 1e-5 relative (north star's FP32 mode) on
+ *              well-conditioned weights.  Volume update / interpolant only.
+ * Any other precision code fails with IM_INVALID_ARGUMENT.
  */
 #ifndef ICEMORPH_B200_H
 #define ICEMORPH_B200_H
@@ -52,6 +57,7 @@ extern "C" {
 
 #define IM_EXACT 0
 #define IM_FP64 1
+#define IM_FP32 2
 
 typedef struct im_context im_context;
 

@@ -22,7 +22,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("IMB_LIB") or os.path.join(HERE, "libicemorph_b200.so")  # IMB_LIB: development override
 KINDS = {"c0": 0, "c2": 1, "c4": 2, "c6": 3}
 PSI = {"linear": 0, "c2": 1, "wendland_c2": 1}
-EXACT, FP64 = 0, 1
+EXACT, FP64, FP32 = 0, 1, 2  # IM_EXACT, IM_FP64, IM_FP32
 
 _sz = C.c_size_t
 _d = C.c_double

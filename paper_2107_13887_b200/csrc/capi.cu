@@ -295,6 +295,7 @@ int im_eval_interpolant(im_context* ctx, const double* ctrl, const double* alpha
                         double* out) {
   return guarded(ctx, [&](Context& c) {
     check_kind(basis.kind);
+    precision_of(precision);
     if (nq == 0) return;
     DPoints q;
     upload_points(c, queries, nq, q);
@@ -322,7 +323,7 @@ int im_eval_interpolant(im_context* ctx, const double* ctrl, const double* alpha
     a.R = basis.support_radius;
     a.kind = basis.kind;
     a.dim = 3;
-    a.precision = exact ? Precision::Exact : Precision::Fast64;
+    a.precision = precision_of(precision);
     a.out_val = dout.p;
     EventTimer tm(c.stream);
     launch_volume(c, a);
@@ -567,6 +568,7 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
   return guarded(ctx, [&](Context& c) {
     PhaseTrace tr(c.stream);
     check_kind(basis.kind);
+    precision_of(precision);
     *n_entries = 0;
     const double D = wf->support_distance;
     if (D <= 0.0 || n_nodes == 0) return;  // wall_distance.cpp:54
@@ -641,7 +643,7 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     a.R = basis.support_radius;
     a.kind = basis.kind;
     a.dim = planar && (!exact || tiled_exact) ? 2 : 3;
-    a.precision = exact ? Precision::Exact : Precision::Fast64;
+    a.precision = precision_of(precision);
     a.exact_tiled = tiled_exact;
     a.ctrl_index = midx, a.index_box = mbox;
     a.ctrl_diag = bbox_diagonal(ctrl, nc);

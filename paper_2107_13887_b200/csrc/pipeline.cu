@@ -156,6 +156,7 @@ struct im_volume_plan {
     DBuf<double> tiles, boxes, midx, mbox;
     bool culled = false;
     bool exact_tiled = false;
+    bool exact_format = false;  // packed for IM_EXACT (insertion-order tiles)
     double diag = 0.0;
     DBuf<uint32_t> order;  // cached longest-first block order (exact kernel)
     size_t order_n = 0;
@@ -365,7 +366,7 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
         a.R = g.basis.support_radius;
         a.kind = g.basis.kind;
         a.dim = planar ? 2 : 3;
-        a.precision = exact ? Precision::Exact : Precision::Fast64;
+        a.precision = precision_of(cfg->precision);
         a.acc_x = acc.x.p, a.acc_y = acc.y.p, a.acc_z = acc.z.p;
         a.pinned = n_pinned ? pinflag.p : nullptr;
         launch_volume(c, a);
@@ -536,7 +537,7 @@ int im_volume_plan_run(im_volume_plan* p, const im_wall_function* wf, im_basis b
     a.R = basis.support_radius;
     a.kind = basis.kind;
     a.dim = p->dim;
-    a.precision = exact ? Precision::Exact : Precision::Fast64;
+    a.precision = precision_of(precision);
     a.exact_tiled = tiled_exact;
     a.ctrl_index = tiled_exact ? midx.p : nullptr;
     a.index_box = tiled_exact ? mbox.p : nullptr;
@@ -597,6 +598,7 @@ int im_volume_plan_set_level(im_volume_plan* p, int level, const double* ctrl, c
                              size_t nc, double D, int psi_kind, im_basis basis, int precision) {
   return guarded(p->ctx, [&](Context& c) {
     if (level < 0 || level >= 8) throw InvalidArgument("level index out of range (0..7)");
+    precision_of(precision);
     const bool tiled_exact =
         precision == IM_EXACT &&
         exact_tiled_ok(basis.support_radius,
@@ -642,6 +644,7 @@ int im_volume_plan_set_level(im_volume_plan* p, int level, const double* ctrl, c
       L.culled = true;
     }
     L.exact_tiled = tiled_exact;
+    L.exact_format = precision == IM_EXACT;
     L.diag = bbox_diagonal(ctrl, nc);
     L.order_n = 0;  // block order recomputed at the next run
     L.host_ctrl.assign(ctrl, ctrl + 3 * nc);
@@ -661,6 +664,10 @@ int im_volume_plan_set_level(im_volume_plan* p, int level, const double* ctrl, c
 int im_volume_plan_run_steps(im_volume_plan* p, im_basis basis, int precision, int steps,
                              int flush_l2, double* stats) {
   return guarded(p->ctx, [&](Context& c) {
+    const Precision prec = precision_of(precision);
+    for (int l = 0; l < p->n_levels; ++l)
+      if (p->levels[l].D > 0.0 && p->levels[l].exact_format != (prec == Precision::Exact))
+        throw InvalidArgument("plan level was set for a different precision (set_level)");
     const size_t flush_bytes = size_t(256) << 20;
     if (flush_l2) p->flush.reserve(flush_bytes);
     cudaEvent_t e0, e1, k0, k1;
@@ -699,7 +706,7 @@ int im_volume_plan_run_steps(im_volume_plan* p, im_basis basis, int precision, i
         a.R = basis.support_radius;
         a.kind = basis.kind;
         a.dim = p->dim;
-        a.precision = precision == IM_EXACT ? Precision::Exact : Precision::Fast64;
+        a.precision = prec;
         a.exact_tiled = L.exact_tiled;
         a.ctrl_index = L.exact_tiled ? L.midx.p : nullptr;
         a.index_box = L.exact_tiled ? L.mbox.p : nullptr;

@@ -165,6 +165,12 @@ void pack_controls_host(Context& ctx, const double* host_ctrl, const double* hos
 void aos_to_soa(Context& ctx, const double* d_aos, size_t n, double* x, double* y, double* z);
 
 enum class Precision : int { Exact = 0, Fast64 = 1, Fast32 = 2 };
+// C-ABI precision code (IM_EXACT / IM_FP64 / IM_FP32) -> Precision
+inline Precision precision_of(int code) {
+  if (code < 0 || code > 2)
+    throw InvalidArgument("unknown precision (expected IM_EXACT, IM_FP64 or IM_FP32)");
+  return static_cast<Precision>(code);
+}
 
 struct VolumeArgs {
   // points (SoA); optional gather list of active node ids (nullptr = identity)

@@ -39,6 +39,14 @@ def _kind(name: str) -> str:
     return name.lower()
 
 
+def _precision(name: str) -> int:
+    """DeformationConfig.precision (additive extension) -> IM_EXACT / IM_FP64 / IM_FP32."""
+    codes = {"exact": capi.EXACT, "fp64": capi.FP64, "fp32": capi.FP32}
+    if name not in codes:
+        raise ValueError(f"unknown precision '{name}' (expected exact, fp64 or fp32)")
+    return codes[name]
+
+
 def eval_basis(kind: str, support_radius: float, distance: float) -> float:
     """bindings.cpp:199-204 -> eval_basis (rbf.cpp:52-54)."""
     lib = capi.load_library()
@@ -120,7 +128,7 @@ class DisplacementField:
 class DeformationConfig:
     """bindings.cpp:87-117 properties (pipeline.hpp:18-23) plus the additive
     fields: support_distance (None = reference D_l = volume_k * target_max_l),
-    psi ('linear' | 'c2'), precision ('exact' | 'fp64')."""
+    psi ('linear' | 'c2'), precision ('exact' | 'fp64' | 'fp32')."""
 
     def __init__(self):
         self.basis = "c2"
@@ -228,7 +236,7 @@ def deform(mesh: Mesh, displacement: DisplacementField, config: DeformationConfi
                           config.levels, config.max_points_per_level, _kind(config.basis),
                           config.support_radius, config.volume_k, D,
                           1 if config.psi in ("c2", "wendland_c2") else 0,
-                          capi.EXACT if config.precision == "exact" else capi.FP64,
+                          _precision(config.precision),
                           elements=mesh._elements,
                           compute_quality=config.compute_quality and mesh.num_elements > 0)
     out = Mesh(mesh.dim, r["nodes"], mesh._markers, mesh._elements, mesh._marker_elements)
