@@ -240,6 +240,8 @@ int im_context_create(im_context** out, int device) {
 int im_context_destroy(im_context* ctx) {
   if (!ctx) return IM_OK;
   if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+  for (cudaStream_t st : ctx->c.side)
+    if (st) cudaStreamDestroy(st);
   delete ctx;
   return IM_OK;
 }
@@ -448,6 +450,208 @@ int im_count_inverted(im_context* ctx, const double* nodes, size_t n_nodes, cons
 struct im_mesh {
   imb::HostMesh m;
 };
+
+namespace imb {
+namespace {
+
+// Node-chunk granularity of the selective upload in im_update_volume
+// (IMB_E2E_CHUNK overrides; 0 selects the single-pass path): meshes below
+// 64k nodes take the single pass; larger ones 64k-node chunks, <= 1024.
+size_t e2e_chunk_nodes(size_t n) {
+  if (const char* e = std::getenv("IMB_E2E_CHUNK")) {
+    const long long v = std::atoll(e);
+    return v <= 0 ? n : std::max<size_t>(std::min(n, (size_t)v), (n + 1023) / 1024);
+  }
+  if (n < (size_t(1) << 16)) return n;
+  return std::max(size_t(1) << 16, (n + 1023) / 1024);
+}
+
+struct EventSet {
+  std::vector<cudaEvent_t> e;
+  explicit EventSet(size_t n) : e(n, nullptr) {
+    for (auto& x : e) IMB_CHECK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  }
+  ~EventSet() {
+    for (auto x : e)
+      if (x) cudaEventDestroy(x);
+  }
+  cudaEvent_t operator[](size_t i) const { return e[i]; }
+};
+
+// im_update_volume with transfers cut to what the update reads and
+// overlapped with the device work.  The reference API hands over the whole
+// mesh on every call, but update_volume only reads the coordinates of nodes
+// with d < D (wall_distance.cpp:56-62):
+//   side stream 0: the distances (the compaction needs only them), then the
+//                  node chunks that hold at least one active node, merged into
+//                  runs (AoS upload + SoA conversion per run);
+//   ctx.stream:    the stable compaction of the whole mesh while the node
+//                  upload has not started, then — once the runs landed — the
+//                  range / planarity reduction over the active nodes, the
+//                  spatial order and ONE volume kernel over all active nodes
+//                  (the single-pass kernel, same block balance);
+//   side stream 1: the active ids right after the compaction (widened to
+//                  size_t on the host while the kernel runs), the values
+//                  after the kernel (direct DMA into page-locked output).
+// Layer-ordered meshes keep their near-wall (active) nodes in a few
+// contiguous runs, so the node upload shrinks to the active fraction
+// (cfg3: ~20 %); any ordering stays correct, it only uploads more.
+void update_volume_selective(Context& c, const double* nodes, size_t n_nodes, const double* dist,
+                             const double* ctrl, const double* alpha, size_t nc,
+                             const im_wall_function* wf, im_basis basis, Precision prec,
+                             size_t* entry_nodes, double* entry_values, size_t* n_entries,
+                             size_t chunk) {
+  PhaseTrace tr(c.stream);
+  const double D = wf->support_distance, R = basis.support_radius;
+  const bool exact = prec == Precision::Exact;
+  cudaStream_t up = c.side_stream(0), down = c.side_stream(1);
+  double* dx = c.buf<double>(Context::kSlotNodesX, n_nodes);
+  double* dy = c.buf<double>(Context::kSlotNodesY, n_nodes);
+  double* dz = c.buf<double>(Context::kSlotNodesZ, n_nodes);
+  double* dd = c.buf<double>(Context::kSlotDist, n_nodes);
+  uint32_t* active = c.buf<uint32_t>(Context::kSlotActive, n_nodes);
+  double* stage = c.buf<double>(Context::kSlotStage, 3 * n_nodes + 6 * nc);
+  EventSet ev(4);  // 0: distances up, 1: nodes up, 2: ids down, 3: kernel done
+  // 1. distances
+  const H2DJob jd{dd, dist, n_nodes * 8};
+  staged_h2d(c, &jd, 1, 192, {}, up);
+  IMB_CHECK(cudaEventRecord(ev[0], up));
+  tr.mark("dist up");
+  // 2. stable compaction of the whole mesh, active count per node chunk
+  IMB_CHECK(cudaStreamWaitEvent(c.stream, ev[0], 0));
+  EventTimer tm(c.stream);
+  const size_t na = compact_active(c, dd, n_nodes, D, active);
+  *n_entries = na;
+  if (na == 0) {
+    c.last_kernel_ms = tm.stop();
+    return;
+  }
+  const size_t n_chunks = (n_nodes + chunk - 1) / chunk;
+  std::vector<size_t> bounds(n_chunks + 1), pos(n_chunks + 1);
+  for (size_t i = 0; i <= n_chunks; ++i) bounds[i] = std::min(n_nodes, i * chunk);
+  active_lower_bounds(c, active, na, bounds.data(), (int)n_chunks + 1, pos.data());
+  // ids down as soon as they exist
+  unsigned char* pin = pinned_out(c, 4 * na + 24 * na + 32);
+  uint32_t* pin_ids = reinterpret_cast<uint32_t*>(pin);
+  double* pin_vals = reinterpret_cast<double*>(pin + ((4 * na + 15) / 16) * 16);
+  IMB_CHECK(cudaEventRecord(ev[2], c.stream));
+  IMB_CHECK(cudaStreamWaitEvent(down, ev[2], 0));
+  IMB_CHECK(cudaMemcpyAsync(pin_ids, active, 4 * na, cudaMemcpyDeviceToHost, down));
+  IMB_CHECK(cudaEventRecord(ev[2], down));
+  // 3. node runs holding active nodes: upload + SoA (side stream 0)
+  size_t uploaded = 0;
+  for (size_t i = 0; i < n_chunks;) {
+    if (pos[i + 1] == pos[i]) {
+      ++i;
+      continue;
+    }
+    size_t j = i + 1;
+    while (j < n_chunks && pos[j + 1] > pos[j]) ++j;
+    const size_t b = bounds[i], m = bounds[j] - b;
+    const H2DJob jn{stage + 3 * b, nodes + 3 * b, m * 24};
+    staged_h2d(c, &jn, 1, 192, {}, up);
+    aos_to_soa(c, stage + 3 * b, m, dx + b, dy + b, dz + b, up);
+    uploaded += m;
+    i = j;
+  }
+  // 4. controls: host packing overlaps the node upload
+  double* tiles = c.buf<double>(Context::kSlotTiles, ctrl_tile_doubles(nc));
+  double *boxes = nullptr, *midx = nullptr, *mbox = nullptr;
+  double ctrl_max = 0.0;
+  for (size_t i = 0; i < 3 * nc; ++i) ctrl_max = std::max(ctrl_max, std::fabs(ctrl[i]));
+  bool ctrl_planar = true;
+  for (size_t i = 0; i < nc && ctrl_planar; ++i)
+    ctrl_planar = ctrl[3 * i + 2] == 0.0 && alpha[3 * i + 2] == 0.0;
+  const bool ctrl_tiled_ok = exact && exact_tiled_ok(R, ctrl_max);
+  if (exact) {
+    double* cs = stage + 3 * n_nodes;
+    if (nc) {
+      IMB_CHECK(cudaMemcpyAsync(cs, ctrl, nc * 24, cudaMemcpyHostToDevice, c.stream));
+      IMB_CHECK(cudaMemcpyAsync(cs + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice, c.stream));
+    }
+    pack_controls_aos(c, cs, cs + 3 * nc, nc, 1.0, tiles);
+    if (ctrl_tiled_ok) {
+      boxes = c.buf<double>(Context::kSlotBoxes, 6 * (ctrl_padded(nc) / kCtrlTile));
+      exact_tile_boxes(c, tiles, nc, 1.0 / R, boxes);
+      midx = c.buf<double>(Context::kSlotIndex, 4 * ctrl_padded(nc));
+      mbox = c.buf<double>(Context::kSlotIndexBox, 6 * (ctrl_padded(nc) / kCtrlTile));
+      pack_exact_index_host(c, ctrl, nc, 1.0 / R, midx, mbox);
+    }
+  } else {
+    boxes = c.buf<double>(Context::kSlotBoxes, 6 * (ctrl_padded(nc) / kCtrlTile));
+    pack_controls_host(c, ctrl, alpha, nc, 1.0 / R, true, tiles, boxes);
+  }
+  IMB_CHECK(cudaEventRecord(ev[1], up));
+  IMB_CHECK(cudaStreamWaitEvent(c.stream, ev[1], 0));
+  // 5. coordinate range / planarity over the active nodes, then one kernel
+  unsigned long long* dmax = c.buf<unsigned long long>(Context::kSlotChunkMax, 2);
+  max_abs_points_async(dx, dy, dz, na, dmax, c.num_sms, c.stream, active);
+  unsigned long long hm[2];
+  IMB_CHECK(cudaMemcpyAsync(hm, dmax, 16, cudaMemcpyDeviceToHost, c.stream));
+  IMB_CHECK(cudaStreamSynchronize(c.stream));
+  double mx, mz;
+  std::memcpy(&mx, &hm[0], 8);
+  std::memcpy(&mz, &hm[1], 8);
+  tr.mark("compact + node runs up");
+  const bool tiled = ctrl_tiled_ok && exact_tiled_ok(R, std::max(mx, ctrl_max));
+  const bool planar = mz == 0.0 && ctrl_planar;
+  uint32_t* perm = nullptr;
+  if (!exact || tiled) {
+    perm = c.buf<uint32_t>(Context::kSlotPerm, na);
+    spatial_order(c, dx, dy, dz, active, na, R, perm);
+  }
+  double* vals = c.buf<double>(Context::kSlotVals, 3 * na);
+  VolumeArgs a;
+  a.x = dx, a.y = dy, a.z = dz;
+  a.active = active;
+  a.n_active = na;
+  a.dist = dd;
+  a.D = D;
+  a.psi_kind = wf->psi_kind;
+  a.tiles = tiles;
+  a.n_ctrl = nc;
+  a.R = R;
+  a.kind = basis.kind;
+  a.dim = planar && (!exact || tiled) ? 2 : 3;
+  a.precision = prec;
+  a.exact_tiled = tiled;
+  a.ctrl_index = tiled ? midx : nullptr;
+  a.index_box = tiled ? mbox : nullptr;
+  a.ctrl_diag = bbox_diagonal(ctrl, nc);
+  a.out_val = vals;
+  a.tile_box = exact && !tiled ? nullptr : boxes;
+  a.perm = perm;
+  launch_volume(c, a);
+  IMB_CHECK(cudaEventRecord(ev[3], c.stream));
+  // 6. values down; the ids are widened on the host meanwhile
+  const bool vals_direct = host_is_pinned(entry_values);
+  IMB_CHECK(cudaStreamWaitEvent(down, ev[3], 0));
+  IMB_CHECK(cudaMemcpyAsync(vals_direct ? entry_values : pin_vals, vals, 24 * na,
+                            cudaMemcpyDeviceToHost, down));
+  IMB_CHECK(cudaEventSynchronize(ev[2]));
+  constexpr size_t kPiece = size_t(1) << 16;
+  const int pieces = (int)((na + kPiece - 1) / kPiece);
+  host_pool(c).run(pieces, [&](int t) {
+    const size_t k0 = (size_t)t * kPiece, k1 = std::min(na, k0 + kPiece);
+    for (size_t k = k0; k < k1; ++k) entry_nodes[k] = pin_ids[k];
+  });
+  c.last_kernel_ms = tm.stop();
+  tr.mark("order + kernel");
+  IMB_CHECK(cudaStreamSynchronize(down));
+  if (!vals_direct)
+    host_pool(c).run(pieces, [&](int t) {
+      const size_t k0 = (size_t)t * kPiece, k1 = std::min(na, k0 + kPiece);
+      std::memcpy(entry_values + 3 * k0, pin_vals + 3 * k0, 24 * (k1 - k0));
+    });
+  tr.mark("values down");
+  if (std::getenv("IMB_TRACE"))
+    std::fprintf(stderr, "[imb]   selective upload: %zu of %zu nodes in %zu-node chunks, %zu active\n",
+                 uploaded, n_nodes, chunk, na);
+}
+
+}  // namespace
+}  // namespace imb
+
 extern "C" {
 
 int im_su2_read(im_context* ctx, const char* path, im_mesh** out) {
@@ -568,10 +772,17 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
   return guarded(ctx, [&](Context& c) {
     PhaseTrace tr(c.stream);
     check_kind(basis.kind);
-    precision_of(precision);
     *n_entries = 0;
     const double D = wf->support_distance;
-    if (D <= 0.0 || n_nodes == 0) return;  // wall_distance.cpp:54
+    if (D <= 0.0 || n_nodes == 0) {  // wall_distance.cpp:54
+      precision_of(precision);
+      return;
+    }
+    const size_t chunk = e2e_chunk_nodes(n_nodes);
+    if (chunk < n_nodes)
+      return update_volume_selective(c, nodes, n_nodes, dist, ctrl, alpha, nc, wf, basis,
+                                     precision_of(precision), entry_nodes, entry_values,
+                                     n_entries, chunk);
     // device buffers come from the context's grow-only slots: no cudaMalloc /
     // cudaFree on this path
     double* dx = c.buf<double>(Context::kSlotNodesX, n_nodes);

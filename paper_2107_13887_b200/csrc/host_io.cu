@@ -100,9 +100,11 @@ namespace {
 constexpr size_t kChunk = 1u << 20;
 constexpr int kMaxEvents = 128;
 
+}  // namespace
+
 // page-locked (cudaHostAlloc / cudaHostRegister) host memory: the DMA engine
 // reads / writes it directly, no staging pass
-bool is_pinned(const void* p) {
+bool host_is_pinned(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();  // clear the sticky-free error of a pageable pointer query
@@ -110,6 +112,10 @@ bool is_pinned(const void* p) {
   }
   return a.type == cudaMemoryTypeHost;
 }
+
+namespace {
+
+bool is_pinned(const void* p) { return host_is_pinned(p); }
 
 HostIOState& state(Context& c) {
   if (!c.io) {
@@ -152,8 +158,12 @@ struct Chunk {
 
 HostPool& host_pool(Context& c) { return state(c).pool; }
 
-void staged_h2d(Context& c, const H2DJob* jobs, int n_jobs, size_t align, const ChunkScan& scan) {
+unsigned char* pinned_out(Context& c, size_t bytes) { return state(c).pin_out.reserve(bytes); }
+
+void staged_h2d(Context& c, const H2DJob* jobs, int n_jobs, size_t align, const ChunkScan& scan,
+                cudaStream_t stream) {
   HostIOState& s = state(c);
+  cudaStream_t st = stream ? stream : c.stream;
   // caller-pinned sources go straight to the copy engine (the optional scan
   // then reads the source in parallel, overlapping the DMA)
   std::vector<H2DJob> staged;
@@ -161,7 +171,7 @@ void staged_h2d(Context& c, const H2DJob* jobs, int n_jobs, size_t align, const 
   for (int j = 0; j < n_jobs; ++j) {
     if (jobs[j].bytes && is_pinned(jobs[j].src)) {
       IMB_CHECK(cudaMemcpyAsync(jobs[j].dst, jobs[j].src, jobs[j].bytes, cudaMemcpyHostToDevice,
-                                c.stream));
+                                st));
       if (scan) {
         const size_t step = std::max(align, kChunk / align * align);
         const int nch = (int)((jobs[j].bytes + step - 1) / step);
@@ -182,7 +192,7 @@ void staged_h2d(Context& c, const H2DJob* jobs, int n_jobs, size_t align, const 
     const ChunkScan remap = scan ? ChunkScan([&](int k, const unsigned char* p, size_t off, size_t len) {
       scan(staged_id[k], p, off, len);
     }) : ChunkScan();
-    return staged_h2d(c, staged.data(), (int)staged.size(), align, remap);
+    return staged_h2d(c, staged.data(), (int)staged.size(), align, remap, stream);
   }
   size_t total = 0;
   for (int j = 0; j < n_jobs; ++j) total += (jobs[j].bytes + 15) & ~size_t(15);
@@ -215,12 +225,12 @@ void staged_h2d(Context& c, const H2DJob* jobs, int n_jobs, size_t align, const 
     if (scan) scan(k.job, dst, k.off, k.len);
     const auto b = std::chrono::steady_clock::now();
     IMB_CHECK(cudaMemcpyAsync(static_cast<unsigned char*>(jb.dst) + k.off, dst, k.len,
-                              cudaMemcpyHostToDevice, c.stream));
+                              cudaMemcpyHostToDevice, st));
     const auto e = std::chrono::steady_clock::now();
     memcpy_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(b - a).count();
     issue_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(e - b).count();
   });
-  IMB_CHECK(cudaEventRecord(s.uploaded, c.stream));
+  IMB_CHECK(cudaEventRecord(s.uploaded, st));
   if (std::getenv("IMB_TRACE")) {
     const auto t1 = std::chrono::steady_clock::now();
     IMB_CHECK(cudaEventSynchronize(s.uploaded));

@@ -65,10 +65,18 @@ struct H2DJob {
 // the job, length).  Chunks of a job start at multiples of `align` bytes.
 using ChunkScan = std::function<void(int, const unsigned char*, size_t, size_t)>;
 
-// Uploads all jobs on ctx.stream (asynchronously w.r.t. the device: the
-// copies are enqueued when this returns).  align: chunk alignment in bytes.
+// Uploads all jobs on `stream` (default ctx.stream; asynchronously w.r.t. the
+// device: the copies are enqueued when this returns).  align: chunk alignment
+// in bytes.
 void staged_h2d(Context& ctx, const H2DJob* jobs, int n_jobs, size_t align = 192,
-                const ChunkScan& scan = {});
+                const ChunkScan& scan = {}, cudaStream_t stream = nullptr);
+
+// page-locked (cudaHostAlloc / cudaHostRegister) host memory
+bool host_is_pinned(const void* p);
+HostPool& host_pool(Context& ctx);
+// the context's pinned download staging buffer (grow-only; callers must not
+// overlap two users)
+unsigned char* pinned_out(Context& ctx, size_t bytes);
 
 struct D2HJob {
   const void* src;  // device

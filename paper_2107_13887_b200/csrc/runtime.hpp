@@ -123,10 +123,18 @@ struct Context {
     kSlotNodesX, kSlotNodesY, kSlotNodesZ, kSlotDist, kSlotActive, kSlotPerm, kSlotVals,
     kSlotTiles, kSlotBoxes, kSlotStage, kSlotCell, kSlotCounts, kSlotStart, kSlotBox,
     kSlotScanA, kSlotScanB, kSlotElemKind, kSlotElemOffset, kSlotElemNodes, kSlotSortKeyA,
-    kSlotSortKeyB, kSlotSortTemp, kSlotIndex, kSlotIndexBox, kSlotBlockOrder, kSlotCount
+    kSlotSortKeyB, kSlotSortTemp, kSlotIndex, kSlotIndexBox, kSlotBlockOrder, kSlotChunkMax,
+    kSlotCount
   };
   DBuf<unsigned char> slots[kSlotCount];
   std::shared_ptr<HostIOState> io;  // created on first staged transfer
+  // side streams of the pipelined C-ABI calls (0: uploads + per-chunk prep,
+  // 1: downloads), created on first use, destroyed with the context
+  cudaStream_t side[2] = {nullptr, nullptr};
+  cudaStream_t side_stream(int i) {
+    if (!side[i]) IMB_CHECK(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
+    return side[i];
+  }
   template <class T>
   T* buf(Slot s, size_t count) {
     return reinterpret_cast<T*>(slots[s].reserve(count * sizeof(T) + 16));
@@ -161,8 +169,20 @@ void pack_controls_host(Context& ctx, const double* host_ctrl, const double* hos
                         double scale, bool sort, DBuf<double>& tiles, DBuf<double>& boxes);
 void pack_controls_host(Context& ctx, const double* host_ctrl, const double* host_alpha, size_t n,
                         double scale, bool sort, double* d_tiles, double* d_boxes);
-// device AoS -> SoA
-void aos_to_soa(Context& ctx, const double* d_aos, size_t n, double* x, double* y, double* z);
+// device AoS -> SoA (on `stream`, default ctx.stream)
+void aos_to_soa(Context& ctx, const double* d_aos, size_t n, double* x, double* y, double* z,
+                cudaStream_t stream = nullptr);
+// Asynchronous max |coordinate| and max |z| of n device SoA points (or of the
+// points active[0..n) when given) on `stream`: d_out[0..1] receive their bit
+// patterns (non-negative doubles order as u64)
+void max_abs_points_async(const double* x, const double* y, const double* z, size_t n,
+                          unsigned long long* d_out, int num_sms, cudaStream_t stream,
+                          const uint32_t* active = nullptr);
+// For each of the m node ids bounds[i] (host), the position of the first
+// active id >= bounds[i] in the ascending device list active[0..na)
+// (synchronous; m <= 1024)
+void active_lower_bounds(Context& ctx, const uint32_t* active, size_t na, const size_t* bounds,
+                         int m, size_t* out);
 
 enum class Precision : int { Exact = 0, Fast64 = 1, Fast32 = 2 };
 // C-ABI precision code (IM_EXACT / IM_FP64 / IM_FP32) -> Precision
@@ -251,6 +271,9 @@ void spatial_order(Context& ctx, const double* x, const double* y, const double*
 void spatial_order(Context& ctx, const double* x, const double* y, const double* z,
                    const uint32_t* active, size_t n, double R, uint32_t* perm);
 void scan_u32_to_u64_async(Context& ctx, const unsigned int* in, size_t n, unsigned long long* out);
+// Grows every scratch slot spatial_order / the exact block order use to the
+// size n needs (so later calls with <= n points never reallocate mid-pipeline)
+void reserve_spatial_order(Context& ctx, size_t n);
 
 // Number of (active node, control) pairs with |r_v - r_c| < R (fast path
 // arithmetic, tiles packed with scale 1/R).

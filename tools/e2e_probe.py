@@ -16,9 +16,19 @@ def main():
     import torch
 
     cache = sys.argv[1] if len(sys.argv) > 1 else "devcache/cfg2_controls.npz"
-    z = np.load(cache)
-    levels = [(z[f"c{l}"], z[f"a{l}"]) for l in range(int(z["n"]))]
     w = W.cfg2()
+    if os.path.exists(cache):
+        z = np.load(cache)
+        levels = [(z[f"c{l}"], z[f"a{l}"]) for l in range(int(z["n"]))]
+    else:  # the reference's own cfg2 selection, seeded alphas (cost is alpha-independent)
+        z = np.load(os.path.join(os.path.dirname(__file__), "..", "tests", "golden",
+                                 "cfg2_reference_selection.npz"))
+        rng = np.random.default_rng(0)
+        pos = w.nodes[w.surface]
+        levels = [(pos[z[f"idx{l}"]], rng.standard_normal((len(z[f"idx{l}"]), 3)) * 1e-3)
+                  for l in range(3)]
+        for _, a in levels:
+            a[:, 2] = 0.0
     ctx = capi.Context(0)
     plan = capi.VolumePlan(ctx, w.nodes, 2, w.surface, cutoff=w.D)
     d = plan.distances()
