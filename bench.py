@@ -133,6 +133,16 @@ def dist_env():
 RAW = {"nc": 4096, "nv": 10_000_000, "R": "inf", "D": "inf"}
 
 
+def ncu_traffic(workload, precision):
+    """Per-launch DRAM bytes of the volume kernel from profiles/ncu_traffic.json."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(f"{workload}/{precision}")
+    except (OSError, ValueError):
+        return None
+
+
 def build_workload(name, scale):
     from paper_2107_13887_b200 import workloads as W
 
@@ -248,6 +258,14 @@ def run_b200(args):
                 else 0 if prec == capi.FP32 else (16 if dim == 3 else 14)}
     if prec == capi.FP32:
         roofline["fp32_lane_ops_per_pair"] = 13 if dim == 3 else 10
+    # DRAM traffic of the dominant kernel: dram__bytes_read.sum +
+    # dram__bytes_write.sum of one launch from the committed `ncu --set full`
+    # capture of this workload / precision (profiles/ncu_traffic.json), when
+    # there is one; ncu cannot run inside the timed process
+    tr = ncu_traffic(wl["name"], args.precision)
+    if tr:
+        roofline["traffic"] = tr["bytes_per_launch"]
+        roofline["traffic_source"] = tr["source"]
 
     # --- e2e through the public C-ABI with host buffers ----------------------
     # inputs and outputs in page-locked host memory (the e2e contract): the
