@@ -415,10 +415,16 @@ __device__ __forceinline__ void better(double& v, int& i, double v2, int i2) {
   if (v2 > v || (v2 == v && i2 < i)) v = v2, i = i2;
 }
 
+// KIND >= 0: the staged pair evaluation of the tiled exact kernels
+// (xt::/exact_eval, common.cuh: four controls per stage, summed in insertion
+// order) -- valid when the host verified |positions| <= 1e100 and R in
+// [1e-100, 1e100] (exact_tiled_ok); KIND < 0: one pair at a time with the
+// full-range __dsqrt_rn / division and a runtime basis switch.
+template <int KIND>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep(GView g) {
   GState& st = *g.st;
   if (st.status != 0) return;
-  __shared__ double ct[kSweepTile][6];
+  __shared__ __align__(16) double ct[kSweepTile][6];
   __shared__ double wv[kSweepThreads / 32], wa[kSweepThreads / 32];
   __shared__ int wi[kSweepThreads / 32];
   __shared__ bool last;
@@ -436,7 +442,18 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(GView g) {
       ct[t][3] = g.ax[m0 + t], ct[t][4] = g.ay[m0 + t], ct[t][5] = g.az[m0 + t];
     }
     __syncthreads();
-    if (live) {
+    if (KIND >= 0) {
+      // every thread runs the loop (dead lanes on a zero point: harmless);
+      // past cnt the last control is repeated, evaluated but not summed
+      const double pxa[1] = {px}, pya[1] = {py}, pza[1] = {pz};
+      double fxa[1] = {fx}, fya[1] = {fy}, fza[1] = {fz};
+      for (int t = 0; t < cnt; t += 4) {
+        const int js[4] = {t, min(t + 1, cnt - 1), min(t + 2, cnt - 1), min(t + 3, cnt - 1)};
+        exact_eval<3, KIND < 0 ? C2 : KIND, 1, 4>(&ct[0][0], js, min(4, cnt - t), pxa, pya, pza,
+                                                  fxa, fya, fza, rR);
+      }
+      fx = fxa[0], fy = fya[0], fz = fza[0];
+    } else if (live) {
       for (int t = 0; t < cnt; ++t) {
         // distance(surface_positions[i], surface_positions[controls[m]])
         const double d = exact::dist(px, py, pz, ct[t][0], ct[t][1], ct[t][2]);
@@ -593,7 +610,14 @@ GView GreedyEngine::view() {
   return g;
 }
 
-void GreedyEngine::set_positions(const double* host_xyz) { upload_points(ctx_, host_xyz, n_, pos_); }
+void GreedyEngine::set_positions(const double* host_xyz) {
+  upload_points(ctx_, host_xyz, n_, pos_);
+  pos_max_abs_ = 0.0;
+  for (size_t i = 0; i < (size_t)n_ * 3; ++i) {
+    const double v = std::fabs(host_xyz[i]);
+    if (!(v <= pos_max_abs_)) pos_max_abs_ = v;  // NaN propagates: no fast sweep
+  }
+}
 
 void GreedyEngine::set_target(const double* host_xyz) { upload_points(ctx_, host_xyz, n_, tgt_); }
 
@@ -607,6 +631,9 @@ void GreedyEngine::target_from_residual() {
 void GreedyEngine::reset(double tol, double target_max, int kind, double R) {
   kind_ = kind;
   R_ = R;
+  const bool staged = !std::getenv("IMB_SWEEP_GENERIC") && kind >= C0 && kind <= C6 &&
+                      exact_tiled_ok(R, pos_max_abs_);
+  sweep_kind_ = staged ? kind : -1;
   GState s{};
   s.tol = tol;
   s.target_max = target_max;
@@ -641,8 +668,15 @@ void GreedyEngine::enqueue_step(bool sweep) {
   const GView g = view();
   k_insert<<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);
   launch_backward(g);
-  if (sweep)
-    k_sweep<<<nblk_, kSweepThreads, 0, ctx_.stream>>>(g);
+  if (sweep && sweep_kind_ >= 0) {
+    switch (sweep_kind_) {
+      case C0: k_sweep<C0><<<nblk_, kSweepThreads, 0, ctx_.stream>>>(g); break;
+      case C2: k_sweep<C2><<<nblk_, kSweepThreads, 0, ctx_.stream>>>(g); break;
+      case C4: k_sweep<C4><<<nblk_, kSweepThreads, 0, ctx_.stream>>>(g); break;
+      default: k_sweep<C6><<<nblk_, kSweepThreads, 0, ctx_.stream>>>(g); break;
+    }
+  } else if (sweep)
+    k_sweep<-1><<<nblk_, kSweepThreads, 0, ctx_.stream>>>(g);
   else
     k_next_in_order<<<1, 1, 0, ctx_.stream>>>(g, n_);
   IMB_LAUNCH_CHECK();

@@ -85,6 +85,8 @@ class GreedyEngine {
   int n_, cap_;
   int kind_ = 1;
   double R_ = 1.0;
+  int sweep_kind_ = -1;       // k_sweep<KIND> staged path, or -1 (generic)
+  double pos_max_abs_ = 0.0;  // max |coordinate| of the surface positions
   int nblk_ = 1;
   size_t bw_smem_ = 0, ins_smem_ = 0;
   int ins_y_smem_ = 0, ins_dg_smem_ = 0;
