@@ -133,6 +133,17 @@ def dist_env():
 RAW = {"nc": 4096, "nv": 10_000_000, "R": "inf", "D": "inf"}
 
 
+def sm_max_mhz(index):
+    """Max SM clock of the GPU (nvidia-smi), else the B200 boost clock."""
+    try:
+        out = subprocess.run(["nvidia-smi", "-i", str(index), "--query-gpu=clocks.max.sm",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=10).stdout
+        return float(out.strip().splitlines()[0])
+    except (OSError, ValueError, IndexError, subprocess.SubprocessError):
+        return 1965.0
+
+
 def ncu_traffic(workload, precision):
     """Per-launch DRAM bytes of the volume kernel from profiles/ncu_traffic.json."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
@@ -199,6 +210,19 @@ def run_b200(args):
                   "greedy_points_per_level": [int(len(l.control_indices)) for l in ml.levels],
                   "greedy_cap_hit": [bool(l.cap_hit) for l in ml.levels],
                   "greedy_seconds_total": round(greedy_s, 4)}
+        # latency roofline of the exact greedy: a level of N_c steps runs the
+        # backward substitution (rbf.cpp:114-120) over sum_k k(k-1)/2
+        # dependent subtractions (3 axes side by side), floor = the measured
+        # 8.02-cycle dependent DSUB latency (tools/fp64_probe.cu)
+        mhz = sm_max_mhz(local)
+        chain = [sum(k * (k - 1) / 2 for k in range(1, len(l.control_indices) + 1)) for l in ml.levels]
+        cyc = [l.elapsed_seconds * mhz * 1e6 / c if c else None for l, c in zip(ml.levels, chain)]
+        greedy["greedy_chain"] = {
+            "dependent_subtractions_per_level": [int(c) for c in chain],
+            "cycles_per_subtraction": [round(c, 2) if c else None for c in cyc],
+            "floor_cycles": 8.02, "clock_mhz": mhz,
+            "frac_of_latency_floor": [round(8.02 / c, 3) if c else None for c in cyc],
+            "note": "whole-level time (insert + chain + sweep) over the chain's dependent subtractions"}
         if cache:
             np.savez(cache, n=len(levels), **{f"c{l}": c for l, (c, _) in enumerate(levels)},
                      **{f"a{l}": a for l, (_, a) in enumerate(levels)})

@@ -44,7 +44,7 @@ namespace imb {
 namespace {
 
 constexpr int kInsertThreads = 1024;
-constexpr int kMaxCap = 8192;  // ring[2] + rr in shared memory
+constexpr int kMaxCap = 8192;  // k_insert: rr + ring[2] in shared memory
 constexpr int kSweepThreads = 64;
 constexpr int kSweepTile = 128;
 
@@ -61,10 +61,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // ---------------------------------------------------------------------------
 // k_insert: greedy.cpp:86-112 / rbf.cpp:71-100
 //
-// Shared memory: rr[cap] (running s_j, then row[j]) | ring[2][cap] (columns
-// m, m+1 of L, streamed by cp.async: every thread copies exactly the rows it
-// owns, so cp.async.wait_group alone orders the copy before its own use) |
-// dg[cap] (diag + reciprocal, staged when g.ins_dg_in_smem).
+// Shared memory: rr[cap] (running s_j, then row[j]) | ring[NR][cap] (columns
+// m .. m+NR-1 of L, streamed by cp.async NR-1 steps ahead: every thread
+// copies exactly the rows it owns, so cp.async.wait_group alone orders the
+// copy before its own use and no barrier guards the ring).  The pivot pair
+// (L_mm, 1/L_mm) of row m is held in a register by m's owner thread, loaded
+// 1024 steps ahead.  Per step the critical path is the owner's division,
+// one barrier and the next owner's mul-sub.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
@@ -73,16 +76,17 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+template <int NR>
 __global__ void __launch_bounds__(kInsertThreads) k_insert(GView g) {
   GState& st = *g.st;
   if (st.status != 0) return;
   extern __shared__ double sh[];
   const size_t cap = g.cap;
-  double* rr = sh;                   // [cap]
-  double* ring = sh + cap;           // [2][cap]
-  double2* dgs = reinterpret_cast<double2*>(sh + ((3 * cap + 1) & ~size_t(1)));  // [cap], 16B-aligned
+  double* rr = sh;          // [cap]
+  double* ring = sh + cap;  // [NR][cap]
   const int tid = threadIdx.x;
   const int k = st.nc;
   const int node = st.next;
@@ -90,11 +94,7 @@ __global__ void __launch_bounds__(kInsertThreads) k_insert(GView g) {
 
   const double px = g.px[node], py = g.py[node], pz = g.pz[node];
   const exact::Recip rR = exact::make_recip(g.R);
-  const double2* dg = g.diag;
-  if (g.ins_dg_in_smem) {
-    for (int j = tid; j < k; j += kInsertThreads) dgs[j] = g.diag[j];
-    dg = dgs;
-  }
+  double2 dm = tid < k ? g.diag[tid] : make_double2(1.0, 1.0);  // pivot of my next row
   // column (greedy.cpp:87-93 / rbf.cpp:167-170): phi(distance(c_m, p_new))
   for (int j = tid; j < k; j += kInsertThreads) {
     const double d = exact::dist(g.cx[j], g.cy[j], g.cz[j], px, py, pz);
@@ -103,36 +103,45 @@ __global__ void __launch_bounds__(kInsertThreads) k_insert(GView g) {
   // Right-looking forward substitution (rbf.cpp:80-87): once row[m] is final,
   // every s_j (j > m) does s_j -= L_jm * row[m], so each s_j receives its
   // subtractions in ascending m exactly as in the reference's inner loop.
-  auto issue = [&](int m) {
-    if (m < k) {
-      const double* col = g.Lt + colstart(m, cap);
-      double* dst = ring + (m & 1) * cap;
-      for (int j = m + 1 + ((tid - (m + 1)) % kInsertThreads + kInsertThreads) % kInsertThreads;
-           j < k; j += kInsertThreads)
-        cp_async8(dst + j, col + (j - m));
+  // Per step every thread walks only its own rows; the first of them past the
+  // issued / updated column and the issued column's start in L are carried
+  // incrementally (no per-step division or colstart product: with 1024
+  // threads the per-step instruction count, not the L2 latency, bounds this
+  // loop).
+  constexpr int T = kInsertThreads;
+  int mi = 0, ji = tid > 0 ? tid : T;  // next column to issue, my first row > mi
+  const double* ci = g.Lt;             // its start, colstart(mi, cap)
+  auto issue_next = [&]() {
+    if (mi < k) {
+      double* dst = ring + (mi & (NR - 1)) * cap;
+      for (int j = ji; j < k; j += T) cp_async8(dst + j, ci + (j - mi));
     }
     cp_async_commit();
+    ci += cap - (size_t)mi;  // colstart(mi + 1) = colstart(mi) + cap - mi
+    ++mi;
+    if (ji == mi) ji += T;
   };
-  issue(0);
+#pragma unroll
+  for (int q = 0; q < NR - 1; ++q) issue_next();
   __syncthreads();
+  int ju = tid > 0 ? tid : T;  // my first row > m
   for (int m = 0; m < k; ++m) {
-    if ((m % kInsertThreads) == tid) {
-      const double2 dm = dg[m];
+    if ((m & (T - 1)) == tid) {
       rr[m] = exact::div_rcp(rr[m], exact::Recip{dm.x, dm.y});  // row[j] = s / lj[j]
+      if (m + T < k) dm = g.diag[m + T];
     }
-    issue(m + 1);
-    cp_async_wait1();  // my copies of column m have landed
+    issue_next();             // column m + NR - 1
+    cp_async_wait<NR - 1>();  // my copies of column m have landed
     __syncthreads();
     const double r = rr[m];
-    const double* lc = ring + (m & 1) * cap;
-    for (int j = m + 1 + ((tid - (m + 1)) % kInsertThreads + kInsertThreads) % kInsertThreads;
-         j < k; j += kInsertThreads)
-      rr[j] = exact::sub(rr[j], exact::mul(lc[j], r));
+    const double* lc = ring + (m & (NR - 1)) * cap;
+    for (int j = ju; j < k; j += T) rr[j] = exact::sub(rr[j], exact::mul(lc[j], r));
+    if (ju == m + 1) ju += T;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   // stage y_0..y_{k-1} for the forward chain in the ring space when it fits
   const double *yxs = g.yx, *yys = g.yy, *yzs = g.yz;
-  if (g.ins_y_in_smem) {
+  if (NR >= 3) {
     double* ys = sh + cap;
     for (int j = tid; j < k; j += kInsertThreads)
       ys[j] = g.yx[j], ys[cap + j] = g.yy[j], ys[2 * cap + j] = g.yz[j];
@@ -573,10 +582,11 @@ GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap
     IMB_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(bw_smem_, 48 * 1024)));
   // k_insert: rr + ring[2] (+ dg staging, which also makes room for y)
-  ins_smem_ = (size_t)cap * 24;
-  if ((size_t)cap * 40 + 16 <= 210 * 1024) ins_smem_ = (size_t)cap * 40 + 16, ins_dg_smem_ = 1;
-  ins_y_smem_ = ins_dg_smem_;
-  IMB_CHECK(cudaFuncSetAttribute(k_insert, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  // k_insert: rr + a ring of 4 columns when it fits (cap <= 5812), else 2
+  ins_ring_ = (size_t)cap * 8 * 5 <= 227 * 1024 && !std::getenv("IMB_INSERT_RING2") ? 4 : 2;
+  ins_smem_ = (size_t)cap * 8 * (1 + ins_ring_);
+  IMB_CHECK(cudaFuncSetAttribute(ins_ring_ == 4 ? k_insert<4> : k_insert<2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)std::max<size_t>(ins_smem_, 48 * 1024)));
 }
 
@@ -605,8 +615,6 @@ GView GreedyEngine::view() {
   g.bv = bv_.p, g.ba = ba_.p, g.bi = bi_.p;
   g.rec_err = rec_err_.p;
   g.rec_sec = rec_sec_.p;
-  g.ins_y_in_smem = ins_y_smem_;
-  g.ins_dg_in_smem = ins_dg_smem_;
   return g;
 }
 
@@ -664,9 +672,16 @@ void GreedyEngine::launch_backward(const GView& g) {
   }
 }
 
+void GreedyEngine::launch_insert(const GView& g) {
+  if (ins_ring_ == 4)
+    k_insert<4><<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);
+  else
+    k_insert<2><<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);
+}
+
 void GreedyEngine::enqueue_step(bool sweep) {
   const GView g = view();
-  k_insert<<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);
+  launch_insert(g);
   launch_backward(g);
   if (sweep && sweep_kind_ >= 0) {
     switch (sweep_kind_) {
@@ -697,7 +712,7 @@ const GState& GreedyEngine::factor_all_and_solve() {
   // to the O(n^2) append at these sizes and keep one code path.
   const GView g = view();
   for (int k = 0; k < n_; ++k) {
-    k_insert<<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);
+    launch_insert(g);
     k_next_in_order<<<1, 1, 0, ctx_.stream>>>(g, n_);
   }
   launch_backward(g);

@@ -46,8 +46,6 @@ struct GView {
   double *bv, *ba;
   int* bi;
   double *rec_err, *rec_sec;
-  int ins_y_in_smem;
-  int ins_dg_in_smem;
 };
 
 class GreedyEngine {
@@ -80,6 +78,7 @@ class GreedyEngine {
   GView view();
   void enqueue_step(bool sweep);
   void launch_backward(const GView& g);
+  void launch_insert(const GView& g);
 
   Context& ctx_;
   int n_, cap_;
@@ -89,7 +88,7 @@ class GreedyEngine {
   double pos_max_abs_ = 0.0;  // max |coordinate| of the surface positions
   int nblk_ = 1;
   size_t bw_smem_ = 0, ins_smem_ = 0;
-  int ins_y_smem_ = 0, ins_dg_smem_ = 0;
+  int ins_ring_ = 2;  // columns of L in flight in k_insert
   DPoints pos_, tgt_, res_, cpos_, y_, alpha_;
   DBuf<unsigned char> sel_;
   DBuf<int> cidx_;
