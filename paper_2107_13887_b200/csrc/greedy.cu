@@ -79,8 +79,8 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int NR>
-__global__ void __launch_bounds__(kInsertThreads) k_insert(GView g) {
+template <int NR, int T = kInsertThreads>
+__global__ void __launch_bounds__(T) k_insert(GView g) {
   GState& st = *g.st;
   if (st.status != 0) return;
   extern __shared__ double sh[];
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kInsertThreads) k_insert(GView g) {
   const exact::Recip rR = exact::make_recip(g.R);
   double2 dm = tid < k ? g.diag[tid] : make_double2(1.0, 1.0);  // pivot of my next row
   // column (greedy.cpp:87-93 / rbf.cpp:167-170): phi(distance(c_m, p_new))
-  for (int j = tid; j < k; j += kInsertThreads) {
+  for (int j = tid; j < k; j += T) {
     const double d = exact::dist(g.cx[j], g.cy[j], g.cz[j], px, py, pz);
     rr[j] = exact::wendland_rt(g.kind, exact::div_rcp(d, rR));
   }
@@ -108,7 +108,6 @@ __global__ void __launch_bounds__(kInsertThreads) k_insert(GView g) {
   // incrementally (no per-step division or colstart product: with 1024
   // threads the per-step instruction count, not the L2 latency, bounds this
   // loop).
-  constexpr int T = kInsertThreads;
   int mi = 0, ji = tid > 0 ? tid : T;  // next column to issue, my first row > mi
   const double* ci = g.Lt;             // its start, colstart(mi, cap)
   auto issue_next = [&]() {
@@ -143,7 +142,7 @@ __global__ void __launch_bounds__(kInsertThreads) k_insert(GView g) {
   const double *yxs = g.yx, *yys = g.yy, *yzs = g.yz;
   if (NR >= 3) {
     double* ys = sh + cap;
-    for (int j = tid; j < k; j += kInsertThreads)
+    for (int j = tid; j < k; j += T)
       ys[j] = g.yx[j], ys[cap + j] = g.yy[j], ys[2 * cap + j] = g.yz[j];
     yxs = ys, yys = ys + cap, yzs = ys + 2 * cap;
   }
@@ -187,7 +186,7 @@ __global__ void __launch_bounds__(kInsertThreads) k_insert(GView g) {
   __syncthreads();
   if (st.status != 0) return;
   // scatter the new row into the columns: L_kj at column j, offset k - j
-  for (int j = tid; j < k; j += kInsertThreads) g.Lt[colstart(j, cap) + (k - j)] = rr[j];
+  for (int j = tid; j < k; j += T) g.Lt[colstart(j, cap) + (k - j)] = rr[j];
 }
 
 // ---------------------------------------------------------------------------
@@ -585,9 +584,10 @@ GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap
   // k_insert: rr + a ring of 4 columns when it fits (cap <= 5812), else 2
   ins_ring_ = (size_t)cap * 8 * 5 <= 227 * 1024 && !std::getenv("IMB_INSERT_RING2") ? 4 : 2;
   ins_smem_ = (size_t)cap * 8 * (1 + ins_ring_);
-  IMB_CHECK(cudaFuncSetAttribute(ins_ring_ == 4 ? k_insert<4> : k_insert<2>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(ins_smem_, 48 * 1024)));
+  if (const char* e = std::getenv("IMB_INSERT_T")) ins_threads_ = std::atoi(e);
+  for (auto kern : {k_insert<4>, k_insert<4, 256>, k_insert<4, 512>, k_insert<2>})
+    IMB_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::max<size_t>(ins_smem_, 48 * 1024)));
 }
 
 GreedyEngine::~GreedyEngine() {
@@ -673,7 +673,11 @@ void GreedyEngine::launch_backward(const GView& g) {
 }
 
 void GreedyEngine::launch_insert(const GView& g) {
-  if (ins_ring_ == 4)
+  if (ins_ring_ == 4 && ins_threads_ == 256)
+    k_insert<4, 256><<<1, 256, ins_smem_, ctx_.stream>>>(g);
+  else if (ins_ring_ == 4 && ins_threads_ == 512)
+    k_insert<4, 512><<<1, 512, ins_smem_, ctx_.stream>>>(g);
+  else if (ins_ring_ == 4)
     k_insert<4><<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);
   else
     k_insert<2><<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);

@@ -89,6 +89,7 @@ class GreedyEngine {
   int nblk_ = 1;
   size_t bw_smem_ = 0, ins_smem_ = 0;
   int ins_ring_ = 2;  // columns of L in flight in k_insert
+  int ins_threads_ = 1024;  // k_insert CTA size
   DPoints pos_, tgt_, res_, cpos_, y_, alpha_;
   DBuf<unsigned char> sel_;
   DBuf<int> cidx_;
