@@ -133,6 +133,32 @@ def dist_env():
 RAW = {"nc": 4096, "nv": 10_000_000, "R": "inf", "D": "inf"}
 
 
+def deform_section(ctx, wl, nodes, dim, surface, R, D, capi):
+    """Total deformation time through the public entry point (im_deform =
+    pipeline.cpp:19-106 deform): host mesh in, exact multilevel greedy, wall
+    distance, per-level volume update and accumulation, deformed mesh out."""
+    try:
+        t0 = time.perf_counter()
+        r = ctx.deform(nodes, dim, surface, wl["disp"], tol=wl["tol"], max_levels=wl["levels"],
+                       cap=wl["cap"], kind="c2", R=R,
+                       support_distance=D if math.isfinite(D) else float("inf"),
+                       psi_kind=wl["psi_kind"], precision=capi.EXACT)
+        wall = time.perf_counter() - t0
+        return {"total_seconds_wall": round(wall, 3), "total_seconds": round(r["total_seconds"], 3),
+                "greedy_seconds": round(r["greedy_seconds"], 3),
+                "distance_seconds": round(r["distance_seconds"], 4),
+                "volume_seconds": round(r["volume_seconds"], 4),
+                "points_per_level": [int(x) for x in r["points"]],
+                "surface_max_error": r["surface_max_error"],
+                "api": "im_deform (deform, pipeline.hpp:54-56), exact precision, host buffers",
+                "reference_cpu_note": "the reference's own run of this workload's greedy took "
+                                      "1.09 / 92.3 / 1531 s per level on one core "
+                                      "(tests/golden/cfg2_reference_selection.npz)"
+                if wl["name"].startswith("cfg2") else None}
+    except Exception as e:  # reported, never fatal to the bench line
+        return {"error": f"{type(e).__name__}: {e}"}
+
+
 def sm_max_mhz(index):
     """Max SM clock of the GPU (nvidia-smi), else the B200 boost clock."""
     try:
@@ -347,6 +373,8 @@ def run_b200(args):
         if wl["fixed_controls"] is not None:  # FP32 mode: well-conditioned weights only
             out["fp32"] = fast_section(args, plan, levels, wl, R, D, pairs_step, fin, in_step,
                                        launches_per_step, world, capi, capi.FP32)
+    if greedy.get("greedy_seconds_per_level") and not args.no_deform:
+        out["deform"] = deform_section(ctx, wl, nodes, dim, surface, R, D, capi)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, levels, d_host, budget_s=args.cpu_seconds)
     if rank == 0:
@@ -504,6 +532,8 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-deform", action="store_true",
+                    help="skip the end-to-end im_deform run (total deformation time)")
     ap.add_argument("--precision", default="exact", choices=["fp64", "exact", "fp32"],
                     help="volume-update arithmetic of the headline: exact (bit-identical to the "
                          "reference, default), fp64 (FMA fast path) or fp32 (FP32 mode)")
