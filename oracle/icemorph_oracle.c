@@ -235,6 +235,58 @@ static int rethrow_conditioning_nodes(const double* pos, const size_t* controls,
   return 2;
 }
 
+/* Threads for the greedy sweep (greedy.cpp:122-143).  The sweep is
+ * independent per surface node; each thread scans a contiguous node range
+ * with the reference's strict '>' and the ranges merge in ascending order
+ * with the same rule, so argmax (lowest index on ties) and the overall max
+ * equal the sequential scan bit for bit.  Used to make full-size 3-D
+ * fixtures in reasonable time; 1 (default) is the plain sequential loop. */
+static int g_sweep_threads = 1;
+void or_set_sweep_threads(int n) { g_sweep_threads = n < 1 ? 1 : (n > 256 ? 256 : n); }
+
+typedef struct {
+  const double *pos, *target, *alpha;
+  const size_t* controls;
+  const char* selected;
+  size_t nc, lo, hi;
+  int kind;
+  double R;
+  double* residual;
+  double max_norm, overall;
+  size_t argmax;
+} sweep_job;
+
+static void* sweep_work(void* p) {
+  sweep_job* j = (sweep_job*)p;
+  const double* pos = j->pos;
+  double max_norm = -1.0, overall = 0.0;
+  size_t argmax = (size_t)-1;
+  for (size_t i = j->lo; i < j->hi; ++i) {
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    for (size_t m = 0; m < j->nc; ++m) {
+      const double phi =
+          or_eval_basis(j->kind, j->R, dist3(pos + 3 * i, pos + 3 * j->controls[m]));
+      if (phi != 0.0) {
+        fx += j->alpha[3 * m] * phi;
+        fy += j->alpha[3 * m + 1] * phi;
+        fz += j->alpha[3 * m + 2] * phi;
+      }
+    }
+    double* r = j->residual + 3 * i;
+    r[0] = j->target[3 * i] - fx;
+    r[1] = j->target[3 * i + 1] - fy;
+    r[2] = j->target[3 * i + 2] - fz;
+    const double nrm = norm3(r[0], r[1], r[2]);
+    if (!j->selected[i] && nrm > max_norm) {
+      max_norm = nrm;
+      argmax = i;
+    }
+    overall = (overall < nrm) ? nrm : overall;
+  }
+  j->max_norm = max_norm, j->overall = overall, j->argmax = argmax;
+  return NULL;
+}
+
 /* greedy.cpp:60-170 */
 int or_greedy_level(const double* pos, const double* target, size_t n, double tol,
                     size_t cap_cfg, int kind, double R, size_t level_index,
@@ -285,6 +337,26 @@ int or_greedy_level(const double* pos, const double* target, size_t n, double to
     /* sweep, greedy.cpp:122-143 */
     double max_norm = -1.0;
     size_t argmax = n;
+    double overall = 0.0;
+    if (g_sweep_threads > 1 && n >= 1024) {
+      const int nt = g_sweep_threads;
+      pthread_t th[256];
+      sweep_job jobs[256];
+      for (int t = 0; t < nt; ++t) {
+        jobs[t] = (sweep_job){pos, target, alpha, controls, selected, nc, n * t / nt,
+                              n * (t + 1) / nt, kind, R, residual, 0.0, 0.0, 0};
+        pthread_create(&th[t], NULL, sweep_work, &jobs[t]);
+      }
+      for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+      for (int t = 0; t < nt; ++t) { /* ascending ranges, strict '>' */
+        if (jobs[t].argmax != (size_t)-1 && jobs[t].max_norm > max_norm) {
+          max_norm = jobs[t].max_norm;
+          argmax = jobs[t].argmax;
+        }
+        overall = (overall < jobs[t].overall) ? jobs[t].overall : overall;
+      }
+      goto swept;
+    }
     for (size_t i = 0; i < n; ++i) {
       double fx = 0.0, fy = 0.0, fz = 0.0;
       for (size_t m = 0; m < nc; ++m) {
@@ -304,11 +376,11 @@ int or_greedy_level(const double* pos, const double* target, size_t n, double to
         argmax = i;
       }
     }
-    double overall = 0.0;
     for (size_t i = 0; i < n; ++i) {
       const double e = norm3(residual[3 * i], residual[3 * i + 1], residual[3 * i + 2]);
       overall = (overall < e) ? e : overall; /* std::max */
     }
+  swept:
     achieved = target_max > 0.0 ? overall / target_max : 0.0;
     if (out_rec_points) out_rec_points[nrec] = nc;
     if (out_rec_error) out_rec_error[nrec] = achieved;

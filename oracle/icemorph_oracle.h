@@ -38,6 +38,8 @@ int or_eval_interpolant(const double* ctrl, const double* alpha, size_t nc, int 
                         double R, const double* q, size_t nq, double* out);
 
 /* greedy.cpp:60-170; arrays sized min(cap, n) by the caller. */
+/* greedy sweep threads (bit-identical to the sequential scan); default 1 */
+void or_set_sweep_threads(int n);
 int or_greedy_level(const double* pos, const double* target, size_t n, double tol,
                     size_t cap, int kind, double R, size_t level_index,
                     size_t* out_idx, double* out_alpha, size_t* out_nc,

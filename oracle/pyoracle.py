@@ -102,6 +102,12 @@ class Oracle:
         getattr(L, p + "eval_wendland").restype = _d
         getattr(L, p + "eval_wendland").argtypes = [C.c_int, _d]
 
+    def set_sweep_threads(self, n: int) -> None:
+        """Port only: threads for the greedy sweep (bit-identical results)."""
+        if self.flavour != "port":
+            raise ValueError("the reference greedy is single-threaded")
+        self.lib.or_set_sweep_threads(C.c_int(int(n)))
+
     # -- helpers ---------------------------------------------------------
     def _fn(self, name):
         return getattr(self.lib, self.p + name)

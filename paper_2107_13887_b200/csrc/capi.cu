@@ -330,7 +330,7 @@ int im_eval_interpolant(im_context* ctx, const double* ctrl, const double* alpha
     EventTimer tm(c.stream);
     launch_volume(c, a);
     c.last_kernel_ms = tm.stop();
-    IMB_CHECK(cudaMemcpy(out, dout.p, nq * 24, cudaMemcpyDeviceToHost));
+    sync_copy(c.stream, out, dout.p, nq * 24, cudaMemcpyDeviceToHost);
   });
 }
 
@@ -760,7 +760,7 @@ int im_build_distance_index(im_context* ctx, const double* nodes, size_t n_nodes
     EventTimer tm(c.stream);
     wall_distance(c, dn, n_nodes, ds, n_surface, dim, INFINITY, d.p);
     c.last_kernel_ms = tm.stop();
-    IMB_CHECK(cudaMemcpy(out, d.p, n_nodes * 8, cudaMemcpyDeviceToHost));
+    sync_copy(c.stream, out, d.p, n_nodes * 8, cudaMemcpyDeviceToHost);
     for (size_t i = 0; i < n_surface; ++i) out[surface[i]] = 0.0;  // wall_distance.cpp:29
   });
 }

@@ -278,9 +278,19 @@ __global__ void __launch_bounds__(64) k_backward_t(GView g) {
   // once solved (s = x[i] at rbf.cpp:115 reads its own slot)
   double* comp = XS_SMEM ? P + 6 * kBwPad : g.xs_global;
   if (n == 0) return;
+  // x_{n-1} = y_{n-1} / L_{n-1,n-1} (rbf.cpp:114-119 with an empty inner
+  // loop) is solved here, before the barrier: the producer's second block
+  // (column n-3) already reads it, before any empty[] handshake orders the
+  // two warps
   for (int j = tid; j < n; j += 64) {
-    comp[j] = g.yx[j], comp[cap + j] = g.yy[j], comp[2 * cap + j] = g.yz[j];
-    comp[3 * cap + j] = g.diag[j].x;
+    double vx = g.yx[j], vy = g.yy[j], vz = g.yz[j];
+    const double dj = g.diag[j].x;
+    if (j == n - 1) {
+      const exact::Recip r = exact::make_recip(dj);
+      vx = exact::div_rcp(vx, r), vy = exact::div_rcp(vy, r), vz = exact::div_rcp(vz, r);
+    }
+    comp[j] = vx, comp[cap + j] = vy, comp[2 * cap + j] = vz;
+    comp[3 * cap + j] = dj;
   }
   if (tid == 0) {
     for (int r = 0; r < kBwRing + 4; ++r) bw_mbar_init(&ringbar[r]);
@@ -346,7 +356,6 @@ __global__ void __launch_bounds__(64) k_backward_t(GView g) {
   } else if (lane < 3) {
     // ---------------- consumer ----------------
     double* cx = comp + (size_t)lane * cap;
-    cx[n - 1] = exact::div_rcp(cx[n - 1], exact::make_recip(dd[n - 1]));  // x_{n-1}
     BwBlock cur{n - 2, 0};
     double s = 0.0, rcp_i = 0.0;
     for (int t = 0; cur.i >= 0; ++t) {

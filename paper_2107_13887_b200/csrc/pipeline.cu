@@ -278,10 +278,13 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
     IMB_CHECK(cudaMemcpyAsync(acc.z.p, dn.z.p, n_nodes * 8, cudaMemcpyDeviceToDevice, c.stream));
     upload_points_indexed(c, nodes, patch, n_patch, ds);
     DBuf<double> dist;
-    DBuf<unsigned long long> pidx;
+    DBuf<unsigned long long> pidx, pinidx;  // separate buffers: patch ids / pinned ids
     DBuf<unsigned char> pinflag;
+    const std::vector<unsigned long long> patch_ids(patch, patch + n_patch),
+        pinned_ids(pinned, pinned + n_pinned);
     dist.reserve(n_nodes);
-    pidx.reserve(std::max(n_patch, n_pinned));
+    pidx.reserve(std::max<size_t>(n_patch, 1));
+    pinidx.reserve(std::max<size_t>(n_pinned, 1));
     pinflag.reserve(n_nodes);
     const bool any_volume = cutoff > 0.0;
     if (any_volume) {
@@ -290,24 +293,33 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
         // (xi = d / inf = 0), so the distances are not needed.
         IMB_CHECK(cudaMemsetAsync(dist.p, 0, n_nodes * 8, c.stream));
       } else {
+        // stream-ordered copies (the context stream is non-blocking, so a
+        // plain cudaMemcpy would not order against the kernels on it); the
+        // host vectors stay alive until the synchronisation below
         wall_distance(c, dn, n_nodes, ds, n_patch, dim, cutoff, dist.p);
-        std::vector<unsigned long long> pi(patch, patch + n_patch);
-        IMB_CHECK(cudaMemcpy(pidx.p, pi.data(), n_patch * 8, cudaMemcpyHostToDevice));
+        IMB_CHECK(cudaMemcpyAsync(pidx.p, patch_ids.data(), n_patch * 8, cudaMemcpyHostToDevice,
+                                  c.stream));
         k_zero_at<<<(n_patch + 255) / 256, 256, 0, c.stream>>>(dist.p, pidx.p, n_patch);
       }
     }
     IMB_CHECK(cudaMemsetAsync(pinflag.p, 0, n_nodes, c.stream));
     if (n_pinned) {
-      std::vector<unsigned long long> pp(pinned, pinned + n_pinned);
-      IMB_CHECK(cudaMemcpy(pidx.p, pp.data(), n_pinned * 8, cudaMemcpyHostToDevice));
-      k_set_flags<<<(n_pinned + 255) / 256, 256, 0, c.stream>>>(pinflag.p, pidx.p, n_pinned);
+      IMB_CHECK(cudaMemcpyAsync(pinidx.p, pinned_ids.data(), n_pinned * 8, cudaMemcpyHostToDevice,
+                                c.stream));
+      k_set_flags<<<(n_pinned + 255) / 256, 256, 0, c.stream>>>(pinflag.p, pinidx.p, n_pinned);
     }
     IMB_CHECK(cudaStreamSynchronize(c.stream));
     const double dist_s = since(t_dist);
 
     // per-level volume update (pipeline.cpp:64-85)
     const auto t_vol = Clock::now();
-    const bool planar = dim == 2 && all_z_zero(nodes, n_nodes);
+    // the 2-D kernels write vz = 0 * psi: only when every node AND every
+    // level's z weight is zero (the reference's DisplacementField is a Vec3,
+    // so a planar mesh may still carry a z displacement)
+    bool planar = dim == 2 && all_z_zero(nodes, n_nodes);
+    for (size_t l = 0; planar && l < levels.size(); ++l)
+      for (size_t i = 0; planar && i < levels[l].idx.size(); ++i)
+        planar = levels[l].alpha[3 * i + 2] == 0.0;
     DBuf<uint32_t> active;
     active.reserve(n_nodes);
     DBuf<double> stage, tiles, boxes, midx, mbox;
@@ -459,7 +471,7 @@ int im_volume_plan_create(im_context* ctx, const double* nodes, size_t n_nodes, 
       DBuf<unsigned long long> pidx;
       pidx.reserve(n_surface);
       std::vector<unsigned long long> pi(surface, surface + n_surface);
-      IMB_CHECK(cudaMemcpy(pidx.p, pi.data(), n_surface * 8, cudaMemcpyHostToDevice));
+      sync_copy(c.stream, pidx.p, pi.data(), n_surface * 8, cudaMemcpyHostToDevice);
       k_zero_at<<<(n_surface + 255) / 256, 256, 0, c.stream>>>(p->dist.p, pidx.p, n_surface);
     }
     c.last_kernel_ms = tm.ms();
@@ -487,8 +499,8 @@ int im_volume_plan_set_controls(im_volume_plan* p, const double* ctrl, const dou
     p->ctrl_stage.reserve(6 * std::max<size_t>(nc, 1));
     p->tiles.reserve(ctrl_tile_doubles(nc));
     if (nc) {
-      IMB_CHECK(cudaMemcpy(p->ctrl_stage.p, ctrl, nc * 24, cudaMemcpyHostToDevice));
-      IMB_CHECK(cudaMemcpy(p->ctrl_stage.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice));
+      sync_copy(c.stream, p->ctrl_stage.p, ctrl, nc * 24, cudaMemcpyHostToDevice);
+      sync_copy(c.stream, p->ctrl_stage.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice);
     }
     p->host_ctrl.assign(ctrl, ctrl + 3 * nc);
     p->host_alpha.assign(alpha, alpha + 3 * nc);
@@ -627,8 +639,8 @@ int im_volume_plan_set_level(im_volume_plan* p, int level, const double* ctrl, c
       DBuf<double> stage;
       stage.reserve(6 * std::max<size_t>(nc, 1));
       if (nc) {
-        IMB_CHECK(cudaMemcpy(stage.p, ctrl, nc * 24, cudaMemcpyHostToDevice));
-        IMB_CHECK(cudaMemcpy(stage.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice));
+        sync_copy(c.stream, stage.p, ctrl, nc * 24, cudaMemcpyHostToDevice);
+        sync_copy(c.stream, stage.p + 3 * nc, alpha, nc * 24, cudaMemcpyHostToDevice);
       }
       pack_controls_aos(c, stage.p, stage.p + 3 * nc, nc, 1.0, L.tiles.p);
       L.culled = tiled_exact;

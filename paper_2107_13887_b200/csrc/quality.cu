@@ -190,17 +190,17 @@ size_t signed_measures(Context& ctx, const double* x, const double* y, const dou
   if (hw[1] != ~0ull) {
     const unsigned long long e = hw[1] >> 2, code = hw[1] & 3;
     int kind = 0;
-    IMB_CHECK(cudaMemcpy(&kind, kinds + e, sizeof(int), cudaMemcpyDeviceToHost));
+    sync_copy(ctx.stream, &kind, kinds + e, sizeof(int), cudaMemcpyDeviceToHost);
     // validate_mesh messages (mesh.cpp:168-185)
     if (code == kBadKind) throw InvalidArgument("element list: unknown element kind");
     if (code == kBadCount)
       throw InvalidArgument(std::string("element list: wrong node count for ") + kind_name(kind));
     unsigned long long o[2] = {0, 0};
-    IMB_CHECK(cudaMemcpy(o, offsets + e, 16, cudaMemcpyDeviceToHost));
+    sync_copy(ctx.stream, o, offsets + e, 16, cudaMemcpyDeviceToHost);
     std::string idx = "?";
     for (unsigned long long k = o[0]; k < o[1]; ++k) {
       unsigned long long v = 0;
-      IMB_CHECK(cudaMemcpy(&v, conn + k, 8, cudaMemcpyDeviceToHost));
+      sync_copy(ctx.stream, &v, conn + k, 8, cudaMemcpyDeviceToHost);
       if (v >= n_nodes) {
         idx = std::to_string(v);
         break;
@@ -230,7 +230,7 @@ size_t signed_measures_from_host(Context& ctx, const double* x, const double* y,
       IMB_CHECK(cudaMemcpyAsync(dconn, conn, n_conn * 8, cudaMemcpyHostToDevice, ctx.stream));
   }
   const size_t inverted = signed_measures(ctx, x, y, z, n_nodes, dk, doff, dconn, n_elem, dout);
-  if (out && n_elem) IMB_CHECK(cudaMemcpy(out, dout, n_elem * 8, cudaMemcpyDeviceToHost));
+  if (out && n_elem) sync_copy(ctx.stream, out, dout, n_elem * 8, cudaMemcpyDeviceToHost);
   return inverted;
 }
 
@@ -521,7 +521,7 @@ QualityStats orthogonality_from_host(Context& ctx, const double* x, const double
   if (measures) dm.reserve(std::max<size_t>(n_elem, 1));
   const QualityStats q = orthogonality_device(ctx, x, y, z, n_nodes, dk, doff, dconn, n_elem, scores,
                                               measures ? dm.p : nullptr);
-  if (measures && n_elem) IMB_CHECK(cudaMemcpy(measures, dm.p, n_elem * 8, cudaMemcpyDeviceToHost));
+  if (measures && n_elem) sync_copy(ctx.stream, measures, dm.p, n_elem * 8, cudaMemcpyDeviceToHost);
   return q;
 }
 

@@ -43,6 +43,15 @@ struct CudaError : std::runtime_error {
 
 #define IMB_LAUNCH_CHECK() IMB_CHECK(cudaGetLastError())
 
+// A copy ordered on `stream` and complete on return.  The library's streams
+// are non-blocking, so a plain cudaMemcpy (legacy default stream) would not
+// order against their kernels.
+inline void sync_copy(cudaStream_t stream, void* dst, const void* src, size_t bytes,
+                      cudaMemcpyKind kind) {
+  IMB_CHECK(cudaMemcpyAsync(dst, src, bytes, kind, stream));
+  IMB_CHECK(cudaStreamSynchronize(stream));
+}
+
 // Owning device buffer (grow-only).
 template <class T>
 struct DBuf {
@@ -234,9 +243,13 @@ void launch_volume(Context& ctx, const VolumeArgs& a);
 double max_abs_points(Context& ctx, const double* x, const double* y, const double* z, size_t n,
                       double* max_abs_z = nullptr);
 // ranges under which the tiled exact kernel's sqrt/division shortcuts are
-// bit-exact: |coordinates| <= 1e100, R in [1e-100, 1e100]
+// bit-exact: |coordinates| <= 1e100, R in [1e-100, 1e100]; and its culling
+// tests (tile / warp boxes in 1/R-scaled coordinates against 1 + 1e-9) are
+// safe: |x| / R <= 1e5 bounds the scaled coordinates' rounding error by
+// ~2e-11 (in R units), far inside the margin, so no control with eta < 1
+// is ever culled.  Outside these ranges the untiled exact kernel runs.
 inline bool exact_tiled_ok(double R, double max_abs) {
-  return R >= 1e-100 && R <= 1e100 && max_abs <= 1e100;
+  return R >= 1e-100 && R <= 1e100 && max_abs <= 1e100 && max_abs <= 1e5 * R;
 }
 // Morton index of the controls for the gathered exact kernel: tiles of 256
 // (cx, cy, cz, insertion index) raw + per-tile boxes scaled by inv_R

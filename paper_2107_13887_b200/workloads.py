@@ -259,6 +259,22 @@ def cfg4(scale: float = 1.0) -> Workload:
                       int(2000 * s), 50, 0.0349, _bend_twist, 40.0, 1e-4, 4, math.inf, 4)
 
 
+def wing_surface_case(name: str):
+    """The surface system of cfg3 / cfg4 without the 20M / 40M-node volume
+    (greedy-only tests and fixtures): (positions, displacement, R, tol,
+    levels), identical to ``cfg3().nodes[cfg3().surface]`` etc."""
+    if name == "cfg3":
+        n_chord, n_span, fn, R, tol, levels, seed = 400, 100, _ridge, 0.5, 1e-3, 3, 3
+    elif name == "cfg4":
+        n_chord, n_span, fn, R, tol, levels, seed = 500, 200, _bend_twist, 40.0, 1e-4, 4, 4
+    else:
+        raise ValueError(name)
+    spts, prof = wing_surface(n_chord, n_span)
+    disp = fn(spts, prof, np.random.default_rng(seed)).reshape(-1, 3)
+    return (np.ascontiguousarray(spts.reshape(-1, 3)), np.ascontiguousarray(disp), R, tol,
+            levels)
+
+
 # ---- volume elements (for count_inverted, quality.cpp:142-148) -------------
 # ElementKind ids (mesh.hpp:15-23)
 QUAD, HEX = 2, 4

@@ -1,0 +1,129 @@
+"""Greedy parity on the full 3-D BASELINE wing surfaces (cfg3: 40k points,
+R = 0.5c; cfg4: 100k points, R = 40 = 10b, the near-singular global-support
+case of SURVEY App. B10).
+
+* prefix: max_points_per_level = 300, 2 levels, against the UNMODIFIED
+  reference (tests/golden/wing_prefix_reference.npz, made by
+  tests/golden/make_wing_selection.py): indices, alpha, convergence record,
+  cap flags, achieved errors and the final residual, all bit for bit;
+* full: the reference's default cap of 5000 (capped levels included) against
+  the threaded plain-C port, itself pinned to the reference on the prefix
+  (tests/golden/wing_full_port.npz).  cfg4 levels 0-1 and cfg3 level 0 by
+  default, every level with IMB_FULL=1.
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from paper_2107_13887_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def _check(m, fx, name, levels):
+    assert len(m.levels) == levels
+    for l, lv in enumerate(m.levels):
+        assert np.array_equal(lv.control_indices, fx[f"{name}_idx{l}"]), f"{name} level {l} indices"
+        assert np.array_equal(lv.alpha, fx[f"{name}_alpha{l}"]), f"{name} level {l} alpha"
+        assert np.array_equal(lv.record_error, fx[f"{name}_rec{l}"]), f"{name} level {l} record"
+        assert lv.cap_hit == bool(fx[f"{name}_cap{l}"]), f"{name} level {l} cap"
+        assert lv.achieved_error == float(fx[f"{name}_ach{l}"])
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_wing_prefix_matches_reference(gpu, name):
+    fx = np.load(os.path.join(GOLDEN, "wing_prefix_reference.npz"))
+    pos, disp, R, tol, _ = W.wing_surface_case(name)
+    m = gpu.run_multilevel(pos, disp, tol, 2, 300, "c2", R)
+    _check(m, fx, name, int(fx[f"{name}_nlevels"]))
+    assert _digest(m.final_residual) == str(fx[f"{name}_residual_sha"])
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_wing_full_selection(gpu, name):
+    path = os.path.join(GOLDEN, "wing_full_port.npz")
+    if not os.path.exists(path):
+        pytest.skip("full-size wing fixture not generated")
+    fx = np.load(path)
+    if f"{name}_nlevels" not in fx and f"{name}_error" not in fx:
+        pytest.skip(f"no full-size {name} fixture")
+    pos, disp, R, tol, levels = W.wing_surface_case(name)
+    if f"{name}_error" in fx:  # the reference raises SolveError: same message
+        with pytest.raises(RuntimeError) as e:
+            gpu.run_multilevel(pos, disp, tol, levels, 5000, "c2", R)
+        assert str(e.value) == str(fx[f"{name}_error"])
+        return
+    full = os.environ.get("IMB_FULL") == "1"
+    nl = int(fx[f"{name}_nlevels"])
+    run = nl if full else min(nl, 2 if name == "cfg4" else 1)
+    m = gpu.run_multilevel(pos, disp, tol, run, 5000, "c2", R)
+    _check(m, fx, name, run)
+    if run == nl:
+        assert _digest(m.final_residual) == str(fx[f"{name}_residual_sha"])
+
+
+def _plan_vs_reference(gpu, oracle, nodes, surface, ctrl, alpha, D, psi_kind, R, cutoff):
+    """bench.py's timed path (resident plan, exact precision, one level) vs
+    the reference update_volume (wall_distance.cpp:46-64) on the plan's own
+    wall distances."""
+    from paper_2107_13887_b200 import capi
+
+    plan = capi.VolumePlan(gpu, nodes, 3 if np.any(nodes[:, 2]) else 2, surface, cutoff=cutoff)
+    try:
+        d = plan.distances()
+        plan.set_level(0, ctrl, alpha, D, psi_kind, "c2", R, capi.EXACT)
+        plan.reset_field()
+        st = plan.run_steps(1, "c2", R, capi.EXACT, flush_l2=False)
+        got = plan.field()
+    finally:
+        plan.close()
+    i0, v0 = oracle.update_volume(nodes, d, ctrl, alpha, D, psi_kind, "c2", R,
+                                  nthreads=os.cpu_count() or 1)
+    assert st["active"][0] == len(i0)
+    expect = np.zeros_like(got)
+    expect[i0] = v0
+    assert np.array_equal(got, expect)
+
+
+def test_plan_cfg2_capped_level_full_size(gpu, oracle):
+    """cfg2's capped level at full size: the reference's own 5000 level-2
+    controls (cfg2_reference_selection.npz) over all 563k active nodes of the
+    1.01M-node mesh, the launch bench.py times."""
+    ref = np.load(os.path.join(GOLDEN, "cfg2_reference_selection.npz"))
+    w = W.cfg2()
+    ctrl = w.nodes[w.surface][ref["idx2"]]
+    alpha = np.random.default_rng(22).standard_normal((len(ctrl), 3)) * 1e3
+    _plan_vs_reference(gpu, oracle, w.nodes, w.surface, ctrl, alpha, w.D, w.psi_kind, w.R, w.D)
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_plan_wing_slice(gpu, oracle, name):
+    """cfg3 / cfg4 at full control size: 5000 wing-surface controls (the
+    full-size fixture's capped level when present) over a 120k-node slice of
+    the volume mesh (every k-th node, plus the wall) -- cfg3 with D = 1c
+    culling, cfg4 with D = inf (every node active, distances unused)."""
+    pos, disp, R, tol, _ = W.wing_surface_case(name)
+    path = os.path.join(GOLDEN, "wing_full_port.npz")
+    fx = np.load(path) if os.path.exists(path) else {}
+    key = f"{name}_idx{1 if name == 'cfg4' else 0}"
+    if key in fx and len(fx[key]) == 5000:
+        idx, alpha = fx[key], fx[key.replace("idx", "alpha")]
+    else:
+        idx = np.random.default_rng(3).choice(len(pos), 5000, replace=False)
+        alpha = np.random.default_rng(4).standard_normal((5000, 3))
+    w = getattr(W, name)()
+    vol = w.nodes[: w.meta["n_volume"]]
+    step = max(1, len(vol) // 120000)
+    nodes = np.ascontiguousarray(np.vstack([vol[::step], pos]))
+    surface = np.arange(len(nodes) - len(pos), len(nodes))
+    D = w.D
+    cutoff = D if np.isfinite(D) else -1.0
+    _plan_vs_reference(gpu, oracle, nodes, surface, pos[idx], alpha, D, w.psi_kind, R, cutoff)

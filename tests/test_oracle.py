@@ -184,3 +184,29 @@ def test_port_matches_reference_random(port, ref):
         p = rng.random((25, 3))
         d = rng.standard_normal((25, 3))
         assert np.array_equal(port.solve_weights(p, d, kind, 0.8), ref.solve_weights(p, d, kind, 0.8))
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_threaded_port_matches_wing_prefix(port, name):
+    """The port with a threaded greedy sweep (used to make the full-size wing
+    fixture) reproduces the reference's own 300-point / 2-level prefix on the
+    full cfg3 / cfg4 surfaces bit for bit (tests/golden/make_wing_selection.py)."""
+    import hashlib
+    import os
+
+    from paper_2107_13887_b200 import workloads as W
+
+    fx = np.load(os.path.join(os.path.dirname(__file__), "golden", "wing_prefix_reference.npz"))
+    pos, disp, R, tol, _ = W.wing_surface_case(name)
+    port.set_sweep_threads(max(2, min(8, os.cpu_count() or 2)))
+    try:
+        m = port.run_multilevel(pos, disp, tol, 2, 300, "c2", R)
+    finally:
+        port.set_sweep_threads(1)
+    assert len(m.levels) == int(fx[f"{name}_nlevels"])
+    for l, lv in enumerate(m.levels):
+        assert np.array_equal(lv.control_indices, fx[f"{name}_idx{l}"])
+        assert np.array_equal(lv.alpha, fx[f"{name}_alpha{l}"])
+        assert np.array_equal(lv.record_error, fx[f"{name}_rec{l}"])
+    dg = hashlib.sha256(np.ascontiguousarray(m.final_residual).tobytes()).hexdigest()
+    assert dg == str(fx[f"{name}_residual_sha"])
