@@ -13,6 +13,48 @@ enum : int {
   kStatusConverged = 1,  // achieved < tolerance (greedy.cpp:146)
   kStatusCapHit = 2,     // cap reached or no candidate left (greedy.cpp:147-151)
   kStatusSolveError = 3, // pivot <= 1e-14 * max_diag (rbf.cpp:92)
+  kStatusWatchdog = 4,   // speculative pipeline: a spin loop timed out (never expected)
+};
+
+// ---- speculative pipeline (greedy_spec.cu) ---------------------------------
+struct __align__(16) SpecCtl {
+  int epoch, abort, abort_step, done;  // polled together as one int4
+  int rb_step, conf, status, final_step;
+  int fail_node, fail_row, ticket, fticket;
+  int hits, misses, late, rollbacks;
+  double achieved, overall, fail_pivot;
+  unsigned long long t0;
+};
+// the words the host loop polls, mirrored into mapped pinned memory
+struct SpecHost {
+  volatile int conf, abort, abort_step, status, done;
+};
+struct SpecView {
+  int n, cap, S, kind;
+  double R, tol, target_max;
+  const double *px, *py, *pz, *tx, *ty, *tz;
+  double *rx, *ry, *rz;
+  double *cx, *cy, *cz;
+  int* cidx;
+  double* Lt;
+  double2* diag;
+  double *yx, *yy, *yz;
+  double* slots;      // [S][3][cap] alpha of step k in slot k % S
+  double* xs_global;  // [S][4][cap] chain workspace when smem is too small
+  double *fax, *fay, *faz;  // predictor alpha
+  int* selstep;       // [n] step at which the node was inserted (INT_MAX: not)
+  int *state, *ins_ep, *chain_ep, *ins_node, *ins_fail, *pred_node;  // [cap + 1]
+  double *pivot, *pred_gap, *exact_gap;                              // [cap + 1]
+  double *bv, *bv2, *ba;
+  int* bi;
+  double *fbv, *fbv2;
+  int* fbi;
+  double *rec_err, *rec_sec;
+  SpecCtl* ctl;
+  SpecHost* host;
+};
+struct SpecStats {
+  long long hits = 0, misses = 0, late = 0, rollbacks = 0;
 };
 
 // Device-resident step state (one per level run).
@@ -60,6 +102,8 @@ class GreedyEngine {
   void target_from_residual();
   void reset(double tol, double target_max, int kind, double R);
   const GState& run_level(int batch = 8);
+  const GState& run_level_spec();
+  const SpecStats& spec_stats() const { return spec_stats_; }
   const GState& factor_all_and_solve();
   const GState& poll();
   double bench_backward(int n, int reps);
@@ -76,6 +120,10 @@ class GreedyEngine {
 
  private:
   GView view();
+  SpecView spec_view();
+  void spec_alloc();
+  void spec_free();
+  int spec_restart_step();
   void enqueue_step(bool sweep);
   void launch_backward(const GView& g);
   void launch_insert(const GView& g);
@@ -98,6 +146,18 @@ class GreedyEngine {
   DBuf<int> bi_;
   DBuf<GState> st_;
   GState* hst_ = nullptr;
+  double tol_ = 0.5, target_max_ = 0.0;
+  // speculative pipeline
+  bool sp_ready_ = false, sp_xs_smem_ = true;
+  int spec_S_ = 32, sp_fnblk_ = 1;
+  size_t sp_server_smem_ = 0, sp_fsolve_smem_ = 0;
+  DBuf<double> sp_slots_, sp_fa_, sp_xs_, sp_dwords_, sp_bv2_, sp_fbv_;
+  DBuf<int> sp_selstep_, sp_words_, sp_fbi_;
+  DBuf<SpecCtl> sp_ctl_;
+  SpecHost* sp_host_ = nullptr;
+  SpecHost* sp_host_dev_ = nullptr;
+  cudaStream_t sp_pred_ = nullptr, sp_chain_ = nullptr;
+  SpecStats spec_stats_;
 };
 
 }  // namespace imb

@@ -1,0 +1,825 @@
+// greedy_spec.cu — the exact greedy level as a speculative pipeline
+// (north-star b, c; reference greedy_level, greedy.cpp:60-170).
+//
+// Why.  Step k of the reference re-solves L^T x = y from scratch
+// (greedy.cpp:106-111 -> rbf.cpp:114-120): ~k^2/2 dependent subtractions
+// whose order fixes alpha's bits, so one step is latency-bound (8-cycle DSUB)
+// and a capped 5000-point level is ~2e10 dependent subtractions (~85 s at the
+// floor).  The chain of step k+1 needs only L's rows 0..k, i.e. the selection
+// c_k -- not alpha_k.  So the selection is PREDICTED from an approximate
+// alpha (a blocked FMA triangular solve + an FMA sweep, both cheap and
+// parallel) and the next rows / chains start at once, many steps deep, each
+// chain on its own SM.  Every step's exact chain and exact sweep still run,
+// in the reference's arithmetic; the exact sweep of step k CONFIRMS the
+// prediction of c_k.  A wrong prediction (rare except at near-ties) rolls the
+// speculative steps back and restarts them from the exact c_k.  Control
+// indices, alpha, residual and convergence record are therefore bit-identical
+// to the non-speculative engine (greedy.cu) and to the reference.
+//
+// Step k (k controls c_0..c_{k-1} selected):
+//   chain(k)   alpha_k = L_k^-T y_k, exact order           [server CTA k % S]
+//   sweep(k)   residual with alpha_k, record[k-1], argmax
+//              c_k (or stop), confirm the prediction        [main stream]
+//   fsolve(k) + fsweep(k)   predicted c_k                   [predictor stream]
+//   insert(k)  L row k, y_k for c_k (exact if sweep(k) already decided,
+//              else the prediction)                          [predictor stream]
+// insert(k) enables chain(k+1).  Chains run in a persistent kernel of S CTAs
+// (one per SM, they spin on per-step flags); alpha_k goes to slot k % S, which
+// chain(k+S) reuses once sweep(k) has consumed it.
+//
+// Protocol words (device): state[k] = EMPTY / predicted node / node|EXACT
+// (atomics decide whether insert(k) or sweep(k) came first); ins_ep[k] /
+// chain_ep[k] = epoch in which insert(k) / chain(k) completed; ctl.epoch is
+// bumped by each rollback and every kernel launched for an older epoch is a
+// no-op; ctl.abort stops speculative work between a misprediction and its
+// rollback.  Every spin loop has a watchdog (status kStatusWatchdog).
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+#include "greedy.hpp"
+#include "greedy_dev.cuh"
+
+namespace imb {
+
+using gdev::better;
+using gdev::colstart;
+using gdev::globaltimer;
+using gdev::ld_volatile;
+
+namespace {
+
+constexpr int kEmpty = -1;
+constexpr int kExactBit = 1 << 30;
+constexpr int kNodeMask = kExactBit - 1;
+constexpr int kSweepT = 64;      // exact sweep CTA (one point per thread)
+constexpr int kSweepTile = 128;  // controls per smem tile
+constexpr int kFastT = 128;      // predictor sweep CTA
+constexpr int kFastTile = 256;
+constexpr unsigned long long kWatchdogNs = 120ull * 1000000000ull;
+
+__device__ __forceinline__ int4 ld_volatile4(const int* p) {
+  int4 w;
+  asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+               : "l"(p)
+               : "memory");
+  return w;
+}
+
+__device__ __forceinline__ void st_volatile(int* p, int v) {
+  asm volatile("st.volatile.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// uniform "is this launch still current" test, decided by thread 0
+__device__ __forceinline__ bool launch_live(const SpecCtl* c, int ep) {
+  __shared__ int s_live;
+  if (threadIdx.x == 0) {
+    const int4 w = ld_volatile4(&c->epoch);
+    s_live = w.x == ep && w.y == 0 && w.w == 0;  // epoch, abort, -, done
+  }
+  __syncthreads();
+  return s_live != 0;
+}
+
+__device__ void host_publish(const SpecView& v) {
+  // mirror of the few words the host loop polls (mapped pinned memory)
+  SpecHost* h = v.host;
+  h->conf = v.ctl->conf;
+  h->abort = v.ctl->abort;
+  h->abort_step = v.ctl->abort_step;
+  h->status = v.ctl->status;
+  __threadfence_system();
+  h->done = v.ctl->done;
+  __threadfence_system();
+}
+
+__device__ void finish(const SpecView& v, int status, int final_step) {
+  SpecCtl* c = v.ctl;
+  c->status = status;
+  c->final_step = final_step;
+  __threadfence();
+  c->done = 1;
+  __threadfence();
+  host_publish(v);
+}
+
+// ---------------------------------------------------------------------------
+// init / rollback
+// ---------------------------------------------------------------------------
+__global__ void k_spec_init(SpecView v) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  for (int i = t; i < v.n; i += stride) v.selstep[i] = INT_MAX;
+  for (int k = t; k <= v.cap; k += stride) {
+    v.state[k] = k == 0 ? (0 | kExactBit) : kEmpty;  // c_0 = surface node 0 (greedy.cpp:115)
+    v.ins_ep[k] = -1, v.chain_ep[k] = -1, v.ins_node[k] = -1, v.ins_fail[k] = 0;
+    v.pred_node[k] = -1;
+    v.pred_gap[k] = -1.0, v.exact_gap[k] = -1.0;
+  }
+  if (t == 0) {
+    SpecCtl c{};
+    c.abort_step = INT_MAX;
+    c.rb_step = 0;
+    c.status = kStatusRunning;
+    *v.ctl = c;
+    SpecHost h{};
+    *v.host = h;
+  }
+}
+
+// mispredicted step r: drop every speculative step >= r (c_r is already
+// EXACT in state[r]), re-stamp the surviving inserts, bump the epoch.
+__global__ void k_spec_rollback(SpecView v) {
+  __shared__ int r, ep;
+  if (threadIdx.x == 0) r = v.ctl->abort_step, ep = v.ctl->epoch + 1;
+  __syncthreads();
+  for (int k = threadIdx.x; k <= v.cap; k += blockDim.x) {
+    if (k >= r) {
+      const int node = v.ins_node[k];
+      if (node >= 0 && v.selstep[node] == k) v.selstep[node] = INT_MAX;
+      v.ins_node[k] = -1, v.ins_ep[k] = -1, v.ins_fail[k] = 0;
+      if (k > r) v.state[k] = kEmpty, v.pred_node[k] = -1;
+    } else {
+      v.ins_ep[k] = ep;
+    }
+    if (k > r) v.chain_ep[k] = -1;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    SpecCtl* c = v.ctl;
+    c->rb_step = r;
+    c->rollbacks += 1;
+    __threadfence();
+    c->epoch = ep;
+    __threadfence();
+    c->abort_step = INT_MAX;
+    c->abort = 0;
+    __threadfence();
+    host_publish(v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// insert(k): the row append for c_k (exact if known, else predicted)
+// ---------------------------------------------------------------------------
+template <int NR, int T>
+__global__ void __launch_bounds__(T) k_spec_insert(SpecView v, int k, int ep) {
+  extern __shared__ double sh[];
+  __shared__ int s_node, s_exact;
+  if (!launch_live(v.ctl, ep)) return;
+  if (threadIdx.x == 0) {
+    int node = -1, exact = 0;
+    if (k == 0 || v.ins_ep[k - 1] == ep) {
+      int cur = ld_volatile(&v.state[k]);
+      if (cur == kEmpty) {
+        const int pn = v.pred_node[k];
+        if (pn >= 0) {
+          const int old = atomicCAS(&v.state[k], kEmpty, pn);
+          cur = old == kEmpty ? pn : old;
+        }
+      }
+      if (cur != kEmpty) {
+        exact = (cur & kExactBit) != 0;
+        node = cur & kNodeMask;
+      }
+    }
+    s_node = node, s_exact = exact;
+    if (k == 0) v.ctl->t0 = globaltimer();
+  }
+  __syncthreads();
+  const int node = s_node;
+  if (node < 0) return;  // no prediction (no candidate left): sweep(k) decides
+  gdev::InsertIO io{v.px, v.py, v.pz, v.tx, v.ty, v.tz, v.cx, v.cy, v.cz, v.Lt, (size_t)v.cap,
+                    v.diag, v.yx, v.yy, v.yz, v.kind, v.R};
+  bool ok;
+  const double pivot = gdev::insert_row<NR, T>(io, k, node, 1.0, sh, &ok);
+  if (threadIdx.x == 0) {
+    v.ins_node[k] = node;
+    v.pivot[k] = pivot;
+    if (ok) {
+      v.cidx[k] = node;
+      v.cx[k] = v.px[node], v.cy[k] = v.py[node], v.cz[k] = v.pz[node];
+      v.selstep[node] = k;
+      __threadfence();
+      st_volatile(&v.ins_ep[k], ep);
+    } else {
+      v.ins_fail[k] = 1;
+      if (s_exact) {  // rbf.cpp:92 on the reference's own selection
+        v.ctl->fail_node = node;
+        v.ctl->fail_row = k;
+        v.ctl->fail_pivot = pivot;
+        finish(v, kStatusSolveError, k);
+      }
+      // predicted: sweep(k) tells whether c_k really is this node
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the predictor: approximate alpha_k and the predicted argmax c_k
+// ---------------------------------------------------------------------------
+// Blocked backward substitution with FMAs (not the reference order): block b
+// of 32 rows takes the dot products of its columns' tails with the solved x
+// (one warp per column), then one warp solves the 32 x 32 diagonal block.
+__global__ void __launch_bounds__(1024) k_fast_solve(SpecView v, int n, int ep) {
+  extern __shared__ double xs[];  // [3][cap]
+  __shared__ double sb[3][32], rc[32];
+  __shared__ double T[32][33];  // T[t][r] = L_{b0+r, b0+t}
+  __shared__ int s_ok;
+  if (!launch_live(v.ctl, ep)) return;
+  if (threadIdx.x == 0) s_ok = ld_volatile(&v.ins_ep[n - 1]) == ep;
+  __syncthreads();
+  if (!s_ok) return;
+  const size_t cap = v.cap;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int b1 = n; b1 > 0; b1 -= 32) {
+    const int b0 = max(0, b1 - 32), nb = b1 - b0;
+    if (warp < nb) {
+      const int i = b0 + warp;
+      const double* col = v.Lt + colstart(i, cap) - i;  // col[j] = L_ji
+      double sx = 0.0, sy = 0.0, sz = 0.0;
+#pragma unroll 4
+      for (int j = b1 + lane; j < n; j += 32) {
+        const double l = col[j];
+        sx = fma(l, xs[j], sx), sy = fma(l, xs[cap + j], sy), sz = fma(l, xs[2 * cap + j], sz);
+      }
+      for (int o = 16; o; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        sz += __shfl_xor_sync(0xffffffffu, sz, o);
+      }
+      if (lane > warp && lane < nb) T[warp][lane] = col[b0 + lane];
+      if (lane == 0) {
+        sb[0][warp] = v.yx[i] - sx, sb[1][warp] = v.yy[i] - sy, sb[2][warp] = v.yz[i] - sz;
+        rc[warp] = v.diag[i].y;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double sx = 0.0, sy = 0.0, sz = 0.0, r = 0.0;
+      if (lane < nb) sx = sb[0][lane], sy = sb[1][lane], sz = sb[2][lane], r = rc[lane];
+      for (int q = nb - 1; q >= 0; --q) {
+        const double xx = __shfl_sync(0xffffffffu, sx * r, q);
+        const double xy = __shfl_sync(0xffffffffu, sy * r, q);
+        const double xz = __shfl_sync(0xffffffffu, sz * r, q);
+        if (lane < q) {
+          const double l = T[lane][q];
+          sx = fma(-l, xx, sx), sy = fma(-l, xy, sy), sz = fma(-l, xz, sz);
+        } else if (lane == q) {
+          xs[b0 + q] = xx, xs[cap + b0 + q] = xy, xs[2 * cap + b0 + q] = xz;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    v.fax[i] = xs[i], v.fay[i] = xs[cap + i], v.faz[i] = xs[2 * cap + i];
+}
+
+__device__ __forceinline__ double fast_wendland(int kind, double eta) {
+  const double u = 1.0 - eta, u2 = u * u;
+  switch (kind) {
+    case C0: return u2;
+    case C2: return u2 * u2 * fma(4.0, eta, 1.0);
+    case C4: return u2 * u2 * u2 * fma(fma(35.0 / 3.0, eta, 6.0), eta, 1.0);
+    default: {
+      const double u4 = u2 * u2;
+      return u4 * u4 * fma(fma(fma(32.0, eta, 25.0), eta, 8.0), eta, 1.0);
+    }
+  }
+}
+
+struct Top2 {
+  double v1, v2;
+  int i1;
+};
+__device__ __forceinline__ Top2 merge2(Top2 a, Top2 b) {
+  Top2 r;
+  if (b.v1 > a.v1 || (b.v1 == a.v1 && b.i1 < a.i1)) {
+    r.v1 = b.v1, r.i1 = b.i1, r.v2 = fmax(a.v1, b.v2);
+  } else {
+    r.v1 = a.v1, r.i1 = a.i1, r.v2 = fmax(a.v2, b.v1);
+  }
+  return r;
+}
+__device__ __forceinline__ Top2 warp_top2(Top2 t) {
+  for (int o = 16; o; o >>= 1) {
+    Top2 u;
+    u.v1 = __shfl_xor_sync(0xffffffffu, t.v1, o);
+    u.v2 = __shfl_xor_sync(0xffffffffu, t.v2, o);
+    u.i1 = __shfl_xor_sync(0xffffffffu, t.i1, o);
+    t = merge2(t, u);
+  }
+  return t;
+}
+
+// Predicted argmax of |E|^2 over the candidates (selstep >= k) with the
+// approximate alpha; FMA arithmetic, one point per thread.
+__global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep) {
+  __shared__ __align__(16) double ct[kFastTile][6];
+  __shared__ Top2 wt[kFastT / 32];
+  __shared__ bool last;
+  if (!launch_live(v.ctl, ep)) return;
+  const int n = v.n;
+  const int i = blockIdx.x * kFastT + threadIdx.x;
+  const bool live = i < n;
+  const double px = live ? v.px[i] : 0.0, py = live ? v.py[i] : 0.0, pz = live ? v.pz[i] : 0.0;
+  const double ir2 = 1.0 / (v.R * v.R);
+  double fx = 0.0, fy = 0.0, fz = 0.0;
+  for (int m0 = 0; m0 < k; m0 += kFastTile) {
+    const int cnt = min(kFastTile, k - m0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += kFastT) {
+      ct[t][0] = v.cx[m0 + t], ct[t][1] = v.cy[m0 + t], ct[t][2] = v.cz[m0 + t];
+      ct[t][3] = v.fax[m0 + t], ct[t][4] = v.fay[m0 + t], ct[t][5] = v.faz[m0 + t];
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int t = 0; t < cnt; ++t) {
+      const double dx = px - ct[t][0], dy = py - ct[t][1], dz = pz - ct[t][2];
+      const double e2 = fma(dx, dx, fma(dy, dy, dz * dz)) * ir2;
+      if (e2 < 1.0) {
+        const double phi = fast_wendland(v.kind, sqrt(e2));
+        fx = fma(ct[t][3], phi, fx), fy = fma(ct[t][4], phi, fy), fz = fma(ct[t][5], phi, fz);
+      }
+    }
+  }
+  Top2 t{-1.0, -1.0, n};
+  if (live && v.selstep[i] >= k) {
+    const double ex = v.tx[i] - fx, ey = v.ty[i] - fy, ez = v.tz[i] - fz;
+    const double q = fma(ex, ex, fma(ey, ey, ez * ez));
+    t.v1 = q >= 0.0 ? q : 0.0;  // NaN -> 0: a candidate always yields a prediction
+    t.i1 = i;
+  }
+  t = warp_top2(t);
+  if ((threadIdx.x & 31) == 0) wt[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kFastT / 32; ++w) t = merge2(t, wt[w]);
+    v.fbv[blockIdx.x] = t.v1, v.fbv2[blockIdx.x] = t.v2, v.fbi[blockIdx.x] = t.i1;
+    __threadfence();
+    last = atomicAdd(&v.ctl->fticket, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  Top2 r{-1.0, -1.0, n};
+  for (int b = 0; b < (int)gridDim.x; ++b)
+    r = merge2(r, Top2{((volatile double*)v.fbv)[b], ((volatile double*)v.fbv2)[b],
+                       ((volatile int*)v.fbi)[b]});
+  v.ctl->fticket = 0;
+  v.pred_gap[k] = r.v1 > 0.0 ? (r.v1 - fmax(r.v2, 0.0)) / r.v1 : -1.0;
+  __threadfence();
+  v.pred_node[k] = (r.v1 >= 0.0 && r.i1 < n) ? r.i1 : -1;
+}
+
+// ---------------------------------------------------------------------------
+// exact sweep(k): greedy.cpp:122-153 with alpha_k from its slot
+// ---------------------------------------------------------------------------
+__global__ void k_spec_wait_chain(SpecView v, int k, int ep) {
+  const unsigned long long t0 = globaltimer();
+  for (;;) {
+    const int4 w = ld_volatile4(&v.ctl->epoch);
+    if (w.x != ep || w.y != 0 || w.w != 0) return;
+    if (ld_volatile(&v.chain_ep[k]) == ep) return;
+    if (globaltimer() - t0 > kWatchdogNs) {
+      finish(v, kStatusWatchdog, k);
+      return;
+    }
+    __nanosleep(500);
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int ep) {
+  __shared__ __align__(16) double ct[kSweepTile][6];
+  __shared__ double wv[kSweepT / 32], wa[kSweepT / 32], wv2[kSweepT / 32];
+  __shared__ int wi[kSweepT / 32];
+  __shared__ bool last;
+  if (!launch_live(v.ctl, ep)) return;
+  const int n = v.n;
+  const int slot = k % v.S;
+  const double* ax = v.slots + (size_t)slot * 3 * v.cap;
+  const double* ay = ax + v.cap;
+  const double* az = ay + v.cap;
+  const int i = blockIdx.x * kSweepT + threadIdx.x;
+  const bool live = i < n;
+  const double px = live ? v.px[i] : 0.0, py = live ? v.py[i] : 0.0, pz = live ? v.pz[i] : 0.0;
+  const exact::Recip rR = exact::make_recip(v.R);
+  double fx = 0.0, fy = 0.0, fz = 0.0;
+  for (int m0 = 0; m0 < k; m0 += kSweepTile) {
+    const int cnt = min(kSweepTile, k - m0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += kSweepT) {
+      ct[t][0] = v.cx[m0 + t], ct[t][1] = v.cy[m0 + t], ct[t][2] = v.cz[m0 + t];
+      ct[t][3] = ax[m0 + t], ct[t][4] = ay[m0 + t], ct[t][5] = az[m0 + t];
+    }
+    __syncthreads();
+    if (KIND >= 0) {
+      const double pxa[1] = {px}, pya[1] = {py}, pza[1] = {pz};
+      double fxa[1] = {fx}, fya[1] = {fy}, fza[1] = {fz};
+      for (int t = 0; t < cnt; t += 4) {
+        const int js[4] = {t, min(t + 1, cnt - 1), min(t + 2, cnt - 1), min(t + 3, cnt - 1)};
+        exact_eval<3, KIND < 0 ? C2 : KIND, 1, 4>(&ct[0][0], js, min(4, cnt - t), pxa, pya, pza,
+                                                  fxa, fya, fza, rR);
+      }
+      fx = fxa[0], fy = fya[0], fz = fza[0];
+    } else if (live) {
+      for (int t = 0; t < cnt; ++t) {
+        const double d = exact::dist(px, py, pz, ct[t][0], ct[t][1], ct[t][2]);
+        const double phi = exact::wendland_rt(v.kind, exact::div_rcp(d, rR));
+        if (phi != 0.0) {
+          fx = exact::add(fx, exact::mul(ct[t][3], phi));
+          fy = exact::add(fy, exact::mul(ct[t][4], phi));
+          fz = exact::add(fz, exact::mul(ct[t][5], phi));
+        }
+      }
+    }
+  }
+  double nv = -1.0, all = 0.0, nv2 = -1.0;
+  int ni = n;
+  if (live) {
+    const double ex = exact::sub(v.tx[i], fx), ey = exact::sub(v.ty[i], fy),
+                 ez = exact::sub(v.tz[i], fz);
+    v.rx[i] = ex, v.ry[i] = ey, v.rz[i] = ez;
+    const double nrm = exact::norm(ex, ey, ez);
+    if (v.selstep[i] >= k) nv = nrm, ni = i;  // not among c_0..c_{k-1}
+    all = nrm;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, nv, o);
+    const double s2 = __shfl_xor_sync(0xffffffffu, nv2, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, ni, o);
+    Top2 a{nv, nv2, ni};
+    a = merge2(a, Top2{v2, s2, i2});
+    nv = a.v1, nv2 = a.v2, ni = a.i1;
+    const double a2 = __shfl_xor_sync(0xffffffffu, all, o);
+    all = (all < a2) ? a2 : all;
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) wv[w] = nv, wi[w] = ni, wa[w] = all, wv2[w] = nv2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Top2 a{nv, nv2, ni};
+    for (int t = 1; t < kSweepT / 32; ++t) {
+      a = merge2(a, Top2{wv[t], wv2[t], wi[t]});
+      all = (all < wa[t]) ? wa[t] : all;
+    }
+    v.bv[blockIdx.x] = a.v1, v.bv2[blockIdx.x] = a.v2, v.bi[blockIdx.x] = a.i1;
+    v.ba[blockIdx.x] = all;
+    __threadfence();
+    last = atomicAdd(&v.ctl->ticket, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  // final block: grid argmax + decision (greedy.cpp:136-152)
+  __threadfence();
+  Top2 r{-1.0, -1.0, n};
+  double ov = 0.0;
+  for (int b = 0; b < (int)gridDim.x; ++b) {
+    r = merge2(r, Top2{((volatile double*)v.bv)[b], ((volatile double*)v.bv2)[b],
+                       ((volatile int*)v.bi)[b]});
+    const double a = ((volatile double*)v.ba)[b];
+    ov = (ov < a) ? a : ov;
+  }
+  SpecCtl* c = v.ctl;
+  c->ticket = 0;
+  const double achieved = v.target_max > 0.0 ? exact::div(ov, v.target_max) : 0.0;
+  v.rec_err[k - 1] = achieved;
+  v.rec_sec[k - 1] = (double)(globaltimer() - c->t0) * 1e-9;
+  v.exact_gap[k] = r.v1 > 0.0 ? (r.v1 - fmax(r.v2, 0.0)) / r.v1 : -1.0;
+  c->achieved = achieved;
+  c->overall = ov;
+  const int mi = r.i1;
+  if (achieved < v.tol) {
+    finish(v, kStatusConverged, k);
+    return;
+  }
+  if (k >= v.cap || mi == n) {
+    finish(v, kStatusCapHit, k);
+    return;
+  }
+  // c_k = mi.  Publish it; if insert(k) already ran on a prediction, check it.
+  const int old = atomicExch(&v.state[k], mi | kExactBit);
+  bool mispredict = false;
+  if (old != kEmpty && !(old & kExactBit)) {
+    if (old == mi) {
+      c->hits += 1;
+      if (ld_volatile(&v.ins_fail[k])) {  // the reference's own c_k fails rbf.cpp:92
+        c->fail_node = mi;
+        c->fail_row = k;
+        c->fail_pivot = v.pivot[k];
+        finish(v, kStatusSolveError, k);
+        return;
+      }
+    } else {
+      mispredict = true;
+      c->misses += 1;
+    }
+  } else {
+    c->late += 1;  // decided before the predictor got there
+  }
+  c->conf = k;
+  if (mispredict) {
+    c->abort_step = k;
+    __threadfence();
+    c->abort = 1;
+  }
+  __threadfence();
+  host_publish(v);
+}
+
+// ---------------------------------------------------------------------------
+// chain server: S persistent CTAs, CTA j runs chain(k) for k = j (mod S)
+// ---------------------------------------------------------------------------
+struct SpecAbort {
+  const SpecCtl* c;
+  int k, ep;
+  __device__ int4 poll_issue() const {
+    int4 w;
+    asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                 : "l"(&c->epoch));
+    return w;
+  }
+  __device__ bool poll_test(int4 w) const { return w.x != ep || (w.y != 0 && w.z < k) || w.w != 0; }
+};
+
+__device__ __forceinline__ int first_step_after(int r, int j, int S) {
+  // smallest k > r, k >= 1, with k % S == j
+  int k = r + 1;
+  k += ((j - k % S) + S) % S;
+  if (k < 1) k += S;
+  return k;
+}
+
+template <bool XS_SMEM>
+__global__ void __launch_bounds__(64) k_chain_server(SpecView v) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ int s_go, s_k, s_ep;
+  const int j = blockIdx.x, S = v.S;
+  int k = first_step_after(0, j, S);
+  int ep_local = 0;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const unsigned long long t0 = globaltimer();
+      int go = 0;
+      for (;;) {
+        const int4 w = ld_volatile4(&v.ctl->epoch);
+        if (w.w != 0) break;  // level done
+        if (w.x != ep_local) {
+          ep_local = w.x;
+          k = first_step_after(ld_volatile(&v.ctl->rb_step), j, S);
+        }
+        if (w.y == 0 && k <= v.cap && ld_volatile(&v.ins_ep[k - 1]) == w.x &&
+            ld_volatile(&v.ctl->conf) >= k - S) {
+          go = 1;
+          s_ep = w.x;
+          break;
+        }
+        if (globaltimer() - t0 > kWatchdogNs) {
+          finish(v, kStatusWatchdog, k);
+          break;
+        }
+        __nanosleep(200);
+      }
+      s_go = go, s_k = k;
+    }
+    __syncthreads();
+    if (!s_go) return;
+    const int kk = s_k, ep = s_ep;
+    double* out = v.slots + (size_t)(kk % S) * 3 * v.cap;
+    gdev::ChainIO io{v.Lt, (size_t)v.cap, v.diag, v.yx, v.yy, v.yz, out, out + v.cap,
+                     out + 2 * v.cap, XS_SMEM ? nullptr : v.xs_global + (size_t)j * 4 * v.cap};
+    const bool done = gdev::chain_solve<XS_SMEM, true>(io, kk, sh, SpecAbort{v.ctl, kk, ep});
+    if (threadIdx.x == 0 && done) {
+      __threadfence();
+      st_volatile(&v.chain_ep[kk], ep);
+      __threadfence();
+      const int4 w = ld_volatile4(&v.ctl->epoch);
+      if (w.x == ep && !(w.y != 0 && w.z < kk)) k = kk + S;  // else redo after the rollback
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host driver
+// ---------------------------------------------------------------------------
+SpecView GreedyEngine::spec_view() {
+  SpecView s{};
+  s.n = n_, s.cap = cap_, s.S = spec_S_, s.kind = kind_;
+  s.R = R_;
+  s.tol = tol_, s.target_max = target_max_;
+  s.px = pos_.x.p, s.py = pos_.y.p, s.pz = pos_.z.p;
+  s.tx = tgt_.x.p, s.ty = tgt_.y.p, s.tz = tgt_.z.p;
+  s.rx = res_.x.p, s.ry = res_.y.p, s.rz = res_.z.p;
+  s.cx = cpos_.x.p, s.cy = cpos_.y.p, s.cz = cpos_.z.p;
+  s.cidx = cidx_.p;
+  s.Lt = lt_.p;
+  s.diag = diag_.p;
+  s.yx = y_.x.p, s.yy = y_.y.p, s.yz = y_.z.p;
+  s.slots = sp_slots_.p;
+  s.xs_global = sp_xs_.p;
+  s.fax = sp_fa_.p, s.fay = sp_fa_.p + cap_, s.faz = sp_fa_.p + 2 * (size_t)cap_;
+  s.selstep = sp_selstep_.p;
+  int* w = sp_words_.p;
+  const size_t m = (size_t)cap_ + 1;
+  s.state = w, s.ins_ep = w + m, s.chain_ep = w + 2 * m, s.ins_node = w + 3 * m,
+  s.ins_fail = w + 4 * m, s.pred_node = w + 5 * m;
+  double* d = sp_dwords_.p;
+  s.pivot = d, s.pred_gap = d + m, s.exact_gap = d + 2 * m;
+  s.bv = bv_.p, s.ba = ba_.p, s.bi = bi_.p;
+  s.bv2 = sp_bv2_.p;
+  s.fbv = sp_fbv_.p, s.fbv2 = sp_fbv_.p + sp_fnblk_, s.fbi = sp_fbi_.p;
+  s.rec_err = rec_err_.p, s.rec_sec = rec_sec_.p;
+  s.ctl = sp_ctl_.p;
+  s.host = sp_host_dev_;
+  return s;
+}
+
+void GreedyEngine::spec_alloc() {
+  if (sp_ready_) return;
+  const char* e = std::getenv("IMB_SPEC_S");
+  spec_S_ = e ? std::max(1, std::atoi(e)) : 32;
+  spec_S_ = std::min(spec_S_, std::max(1, ctx_.num_sms - 20));
+  const size_t m = (size_t)cap_ + 1;
+  sp_slots_.reserve((size_t)spec_S_ * 3 * cap_);
+  sp_fa_.reserve(3 * (size_t)cap_);
+  sp_selstep_.reserve(n_);
+  sp_words_.reserve(6 * m);
+  sp_dwords_.reserve(3 * m);
+  sp_bv2_.reserve(nblk_);
+  sp_fnblk_ = (n_ + 127) / 128;
+  sp_fbv_.reserve(2 * (size_t)sp_fnblk_);
+  sp_fbi_.reserve(sp_fnblk_);
+  sp_ctl_.reserve(1);
+  IMB_CHECK(cudaHostAlloc(&sp_host_, sizeof(SpecHost), cudaHostAllocMapped));
+  IMB_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sp_host_dev_), sp_host_, 0));
+  // chain server smem: x / D in shared memory when it fits, else global
+  const size_t head = gdev::chain_smem_head();
+  sp_xs_smem_ = (size_t)cap_ * 32 + head <= 226 * 1024;
+  sp_server_smem_ = sp_xs_smem_ ? (size_t)cap_ * 32 + head : head;
+  if (!sp_xs_smem_) sp_xs_.reserve((size_t)spec_S_ * 4 * cap_);
+  IMB_CHECK(cudaFuncSetAttribute(k_chain_server<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(sp_server_smem_, 48 * 1024)));
+  IMB_CHECK(cudaFuncSetAttribute(k_chain_server<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(sp_server_smem_, 48 * 1024)));
+  sp_fsolve_smem_ = 3 * (size_t)cap_ * 8;
+  IMB_CHECK(cudaFuncSetAttribute(k_fast_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(sp_fsolve_smem_, 48 * 1024)));
+  for (auto kern : {k_spec_insert<4, 1024>, k_spec_insert<2, 1024>})
+    IMB_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::max<size_t>(ins_smem_, 48 * 1024)));
+  int lo, hi;
+  IMB_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  IMB_CHECK(cudaStreamCreateWithPriority(&sp_pred_, cudaStreamNonBlocking, hi));
+  IMB_CHECK(cudaStreamCreateWithPriority(&sp_chain_, cudaStreamNonBlocking, lo));
+  sp_ready_ = true;
+}
+
+void GreedyEngine::spec_free() {
+  if (sp_host_) cudaFreeHost(sp_host_);
+  if (sp_pred_) cudaStreamDestroy(sp_pred_);
+  if (sp_chain_) cudaStreamDestroy(sp_chain_);
+  sp_host_ = nullptr, sp_pred_ = nullptr, sp_chain_ = nullptr;
+}
+
+const GState& GreedyEngine::run_level_spec() {
+  spec_alloc();
+  cudaStream_t sm = ctx_.stream, sp = sp_pred_, sc = sp_chain_;
+  // the level's state (reset() already cleared GState / sel on the main stream)
+  const SpecView v = spec_view();
+  k_spec_init<<<std::max(1, std::min(ctx_.num_sms, (n_ + 255) / 256)), 256, 0, sm>>>(v);
+  IMB_CHECK(cudaStreamSynchronize(sm));
+  // server first, so all S CTAs are resident before anything else runs
+  if (sp_xs_smem_)
+    k_chain_server<true><<<spec_S_, 64, sp_server_smem_, sc>>>(v);
+  else
+    k_chain_server<false><<<spec_S_, 64, sp_server_smem_, sc>>>(v);
+  IMB_LAUNCH_CHECK();
+  volatile SpecHost* h = sp_host_;
+  const int S = spec_S_;
+  const int fgrid = sp_fnblk_;
+  auto launch_insert = [&](int k, int ep) {
+    if (ins_ring_ == 4)
+      k_spec_insert<4, 1024><<<1, 1024, ins_smem_, sp>>>(v, k, ep);
+    else
+      k_spec_insert<2, 1024><<<1, 1024, ins_smem_, sp>>>(v, k, ep);
+  };
+  auto launch_sweep = [&](int k, int ep) {
+    k_spec_wait_chain<<<1, 1, 0, sm>>>(v, k, ep);
+    switch (sweep_kind_) {
+      case C0: k_spec_sweep<C0><<<nblk_, kSweepT, 0, sm>>>(v, k, ep); break;
+      case C2: k_spec_sweep<C2><<<nblk_, kSweepT, 0, sm>>>(v, k, ep); break;
+      case C4: k_spec_sweep<C4><<<nblk_, kSweepT, 0, sm>>>(v, k, ep); break;
+      case C6: k_spec_sweep<C6><<<nblk_, kSweepT, 0, sm>>>(v, k, ep); break;
+      default: k_spec_sweep<-1><<<nblk_, kSweepT, 0, sm>>>(v, k, ep); break;
+    }
+  };
+  int ep = 0, next = 0;  // next step whose predictor / insert work is to be enqueued
+  const int la = S + 2;  // lookahead in steps beyond the last confirmed one
+  const auto t_start = std::chrono::steady_clock::now();
+  for (;;) {
+    const int conf = h->conf;
+    while (next <= cap_ && next <= conf + la && !h->abort && !h->done) {
+      if (next >= 1) {
+        if (next < cap_) {  // the prediction of c_next feeds insert(next)
+          k_fast_solve<<<1, 1024, sp_fsolve_smem_, sp>>>(v, next, ep);
+          k_fast_sweep<<<fgrid, kFastT, 0, sp>>>(v, next, ep);
+        }
+        launch_sweep(next, ep);
+      }
+      if (next < cap_) launch_insert(next, ep);
+      IMB_LAUNCH_CHECK();
+      ++next;
+    }
+    if (h->done) break;
+    if (h->abort) {
+      IMB_CHECK(cudaStreamSynchronize(sp));
+      IMB_CHECK(cudaStreamSynchronize(sm));
+      if (h->done) break;
+      k_spec_rollback<<<1, 1024, 0, sm>>>(v);
+      IMB_CHECK(cudaStreamSynchronize(sm));
+      ++ep;
+      // restart at the mispredicted step r: sweep(r) is done (c_r is EXACT in
+      // state[r]), so only insert(r) is re-issued, then steps r+1.. as usual
+      const int r = spec_restart_step();
+      launch_insert(r, ep);
+      IMB_LAUNCH_CHECK();
+      next = r + 1;
+      continue;
+    }
+    if (std::chrono::steady_clock::now() - t_start > std::chrono::seconds(3600))
+      throw std::runtime_error("speculative greedy: host watchdog");
+    std::this_thread::yield();
+  }
+  IMB_CHECK(cudaStreamSynchronize(sm));
+  IMB_CHECK(cudaStreamSynchronize(sp));
+  IMB_CHECK(cudaStreamSynchronize(sc));
+  IMB_LAUNCH_CHECK();
+  // results -> the engine's buffers / GState
+  SpecCtl c;
+  IMB_CHECK(cudaMemcpy(&c, sp_ctl_.p, sizeof c, cudaMemcpyDeviceToHost));
+  if (c.status == kStatusWatchdog) throw std::runtime_error("speculative greedy: device watchdog");
+  const int fs = c.final_step;
+  GState& s = *hst_;
+  s = GState{};
+  s.status = c.status;
+  s.achieved = c.achieved;
+  s.overall = c.overall;
+  s.tol = tol_;
+  s.target_max = target_max_;
+  if (c.status == kStatusSolveError) {
+    s.nc = fs;  // c_0..c_{fs-1} inserted, node fail_node failed at row fs
+    s.steps = fs;
+    s.fail_node = c.fail_node;
+    s.fail_row = c.fail_row;
+    s.fail_pivot = c.fail_pivot;
+  } else {
+    s.nc = fs;
+    s.steps = fs;
+    const double* a = sp_slots_.p + (size_t)(fs % S) * 3 * cap_;
+    IMB_CHECK(cudaMemcpyAsync(alpha_.x.p, a, fs * 8, cudaMemcpyDeviceToDevice, sm));
+    IMB_CHECK(cudaMemcpyAsync(alpha_.y.p, a + cap_, fs * 8, cudaMemcpyDeviceToDevice, sm));
+    IMB_CHECK(cudaMemcpyAsync(alpha_.z.p, a + 2 * (size_t)cap_, fs * 8, cudaMemcpyDeviceToDevice, sm));
+  }
+  IMB_CHECK(cudaMemcpyAsync(st_.p, hst_, sizeof(GState), cudaMemcpyHostToDevice, sm));
+  IMB_CHECK(cudaStreamSynchronize(sm));
+  spec_stats_.hits += c.hits, spec_stats_.misses += c.misses, spec_stats_.late += c.late;
+  spec_stats_.rollbacks += c.rollbacks;
+  if (std::getenv("IMB_SPEC_LOG")) {
+    const size_t m = (size_t)cap_ + 1;
+    std::vector<double> pg(m), eg(m);
+    std::vector<int> words(6 * m);
+    IMB_CHECK(cudaMemcpy(pg.data(), sp_dwords_.p + m, m * 8, cudaMemcpyDeviceToHost));
+    IMB_CHECK(cudaMemcpy(eg.data(), sp_dwords_.p + 2 * m, m * 8, cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[spec] n=%d cap=%d S=%d steps=%d hits=%d misses=%d late=%d rollbacks=%d\n",
+                 n_, cap_, S, fs, c.hits, c.misses, c.late, c.rollbacks);
+    if (FILE* f = std::fopen(std::getenv("IMB_SPEC_LOG"), "a")) {
+      std::fprintf(f, "# level n=%d cap=%d steps=%d hits=%d misses=%d late=%d rollbacks=%d\n", n_,
+                   cap_, fs, c.hits, c.misses, c.late, c.rollbacks);
+      for (int k = 1; k <= fs; ++k) std::fprintf(f, "%d %.3e %.3e\n", k, pg[k], eg[k]);
+      std::fclose(f);
+    }
+  }
+  return *hst_;
+}
+
+int GreedyEngine::spec_restart_step() {
+  SpecCtl c;
+  IMB_CHECK(cudaMemcpy(&c, sp_ctl_.p, sizeof c, cudaMemcpyDeviceToHost));
+  return c.rb_step;
+}
+
+}  // namespace imb

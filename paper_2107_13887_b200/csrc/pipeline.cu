@@ -164,6 +164,7 @@ struct im_volume_plan {
     size_t nc = 0;
     double D = 0.0;
     int psi_kind = 0;
+    bool planar = false;  // 2-D kernels: planar mesh, controls and z weights
   };
   Level levels[8];
   int n_levels = 0;
@@ -175,6 +176,14 @@ struct im_volume_plan {
   bool reordered = false;
   DBuf<unsigned char> flush;
 };
+
+// the 2-D kernels take z == 0 for nodes and controls and write vz = 0:
+// only valid when every control's z and z weight are zero as well
+bool planar_controls(const double* ctrl, const double* alpha, size_t nc) {
+  for (size_t i = 0; i < nc; ++i)
+    if (ctrl[3 * i + 2] != 0.0 || alpha[3 * i + 2] != 0.0) return false;
+  return true;
+}
 
 double max_abs_host(const double* v, size_t n) {
   double m = 0.0;
@@ -548,7 +557,7 @@ int im_volume_plan_run(im_volume_plan* p, const im_wall_function* wf, im_basis b
     a.n_ctrl = p->nc;
     a.R = basis.support_radius;
     a.kind = basis.kind;
-    a.dim = p->dim;
+    a.dim = p->dim == 2 && planar_controls(p->host_ctrl.data(), p->host_alpha.data(), p->nc) ? 2 : 3;
     a.precision = precision_of(precision);
     a.exact_tiled = tiled_exact;
     a.ctrl_index = tiled_exact ? midx.p : nullptr;
@@ -632,6 +641,7 @@ int im_volume_plan_set_level(im_volume_plan* p, int level, const double* ctrl, c
     }
     auto& L = p->levels[level];
     L.nc = nc;
+    L.planar = p->dim == 2 && planar_controls(ctrl, alpha, nc);
     L.D = D;
     L.psi_kind = psi_kind;
     if (precision == IM_EXACT) {
@@ -717,7 +727,7 @@ int im_volume_plan_run_steps(im_volume_plan* p, im_basis basis, int precision, i
         a.n_ctrl = L.nc;
         a.R = basis.support_radius;
         a.kind = basis.kind;
-        a.dim = p->dim;
+        a.dim = L.planar ? 2 : 3;
         a.precision = prec;
         a.exact_tiled = L.exact_tiled;
         a.ctrl_index = L.exact_tiled ? L.midx.p : nullptr;
