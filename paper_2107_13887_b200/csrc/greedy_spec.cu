@@ -63,7 +63,7 @@ constexpr int kSweepT = 64;      // exact sweep CTA (one point per thread)
 constexpr int kSweepTile = 128;  // controls per smem tile
 constexpr int kFastT = 128;      // predictor sweep CTA
 constexpr int kFastTile = 256;
-constexpr unsigned long long kWatchdogNs = 120ull * 1000000000ull;
+constexpr unsigned long long kWatchdogNs = 60ull * 1000000000ull;
 
 __device__ __forceinline__ int4 ld_volatile4(const int* p) {
   int4 w;
@@ -323,18 +323,24 @@ __device__ __forceinline__ Top2 warp_top2(Top2 t) {
 
 // Predicted argmax of |E|^2 over the candidates (selstep >= k) with the
 // approximate alpha; FMA arithmetic, one point per thread.
+//
+// Grid-wide ticket kernels (this one and the exact sweep) never leave a block
+// early: the launch-live flags can flip to dead mid-kernel (an abort / done
+// raised on the other stream), so a dead block skips its work but still takes
+// its ticket, and the last block -- which then also sees the launch dead (the
+// flags are monotone within an epoch) -- resets the ticket and returns.
 __global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep) {
   __shared__ __align__(16) double ct[kFastTile][6];
   __shared__ Top2 wt[kFastT / 32];
   __shared__ bool last;
-  if (!launch_live(v.ctl, ep)) return;
+  const bool live_blk = launch_live(v.ctl, ep);
   const int n = v.n;
   const int i = blockIdx.x * kFastT + threadIdx.x;
   const bool live = i < n;
   const double px = live ? v.px[i] : 0.0, py = live ? v.py[i] : 0.0, pz = live ? v.pz[i] : 0.0;
   const double ir2 = 1.0 / (v.R * v.R);
   double fx = 0.0, fy = 0.0, fz = 0.0;
-  for (int m0 = 0; m0 < k; m0 += kFastTile) {
+  for (int m0 = 0; live_blk && m0 < k; m0 += kFastTile) {
     const int cnt = min(kFastTile, k - m0);
     __syncthreads();
     for (int t = threadIdx.x; t < cnt; t += kFastT) {
@@ -371,11 +377,15 @@ __global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep
   __syncthreads();
   if (!last || threadIdx.x != 0) return;
   __threadfence();
+  v.ctl->fticket = 0;
+  {
+    const int4 w = ld_volatile4(&v.ctl->epoch);
+    if (w.x != ep || w.y != 0 || w.w != 0) return;
+  }
   Top2 r{-1.0, -1.0, n};
   for (int b = 0; b < (int)gridDim.x; ++b)
     r = merge2(r, Top2{((volatile double*)v.fbv)[b], ((volatile double*)v.fbv2)[b],
                        ((volatile int*)v.fbi)[b]});
-  v.ctl->fticket = 0;
   v.pred_gap[k] = r.v1 > 0.0 ? (r.v1 - fmax(r.v2, 0.0)) / r.v1 : -1.0;
   __threadfence();
   v.pred_node[k] = (r.v1 >= 0.0 && r.i1 < n) ? r.i1 : -1;
@@ -404,7 +414,7 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
   __shared__ double wv[kSweepT / 32], wa[kSweepT / 32], wv2[kSweepT / 32];
   __shared__ int wi[kSweepT / 32];
   __shared__ bool last;
-  if (!launch_live(v.ctl, ep)) return;
+  const bool live_blk = launch_live(v.ctl, ep);  // see k_fast_sweep on the ticket
   const int n = v.n;
   const int slot = k % v.S;
   const double* ax = v.slots + (size_t)slot * 3 * v.cap;
@@ -415,7 +425,7 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
   const double px = live ? v.px[i] : 0.0, py = live ? v.py[i] : 0.0, pz = live ? v.pz[i] : 0.0;
   const exact::Recip rR = exact::make_recip(v.R);
   double fx = 0.0, fy = 0.0, fz = 0.0;
-  for (int m0 = 0; m0 < k; m0 += kSweepTile) {
+  for (int m0 = 0; live_blk && m0 < k; m0 += kSweepTile) {
     const int cnt = min(kSweepTile, k - m0);
     __syncthreads();
     for (int t = threadIdx.x; t < cnt; t += kSweepT) {
@@ -446,7 +456,7 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
   }
   double nv = -1.0, all = 0.0, nv2 = -1.0;
   int ni = n;
-  if (live) {
+  if (live && live_blk) {
     const double ex = exact::sub(v.tx[i], fx), ey = exact::sub(v.ty[i], fy),
                  ez = exact::sub(v.tz[i], fz);
     v.rx[i] = ex, v.ry[i] = ey, v.rz[i] = ez;
@@ -492,6 +502,10 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
   }
   SpecCtl* c = v.ctl;
   c->ticket = 0;
+  {
+    const int4 w = ld_volatile4(&c->epoch);
+    if (w.x != ep || w.y != 0 || w.w != 0) return;
+  }
   const double achieved = v.target_max > 0.0 ? exact::div(ov, v.target_max) : 0.0;
   v.rec_err[k - 1] = achieved;
   v.rec_sec[k - 1] = (double)(globaltimer() - c->t0) * 1e-9;
@@ -771,7 +785,21 @@ const GState& GreedyEngine::run_level_spec() {
   // results -> the engine's buffers / GState
   SpecCtl c;
   IMB_CHECK(cudaMemcpy(&c, sp_ctl_.p, sizeof c, cudaMemcpyDeviceToHost));
-  if (c.status == kStatusWatchdog) throw std::runtime_error("speculative greedy: device watchdog");
+  if (c.status == kStatusWatchdog) {
+    // diagnostics: the protocol words around the stuck step
+    const size_t m = (size_t)cap_ + 1;
+    std::vector<int> w(6 * m);
+    IMB_CHECK(cudaMemcpy(w.data(), sp_words_.p, w.size() * 4, cudaMemcpyDeviceToHost));
+    std::fprintf(stderr,
+                 "[spec] watchdog: epoch=%d abort=%d abort_step=%d done=%d rb=%d conf=%d "
+                 "final=%d hits=%d misses=%d late=%d rollbacks=%d\n",
+                 c.epoch, c.abort, c.abort_step, c.done, c.rb_step, c.conf, c.final_step, c.hits,
+                 c.misses, c.late, c.rollbacks);
+    for (int k = std::max(0, c.conf - 2); k <= std::min(cap_, c.conf + 6); ++k)
+      std::fprintf(stderr, "[spec]  k=%d state=%x ins_ep=%d chain_ep=%d ins_node=%d ins_fail=%d pred=%d\n",
+                   k, w[k], w[m + k], w[2 * m + k], w[3 * m + k], w[4 * m + k], w[5 * m + k]);
+    throw std::runtime_error("speculative greedy: device watchdog");
+  }
   const int fs = c.final_step;
   GState& s = *hst_;
   s = GState{};
