@@ -24,10 +24,13 @@ struct __align__(16) SpecCtl {
   int hits, misses, late, rollbacks;
   double achieved, overall, fail_pivot;
   unsigned long long t0;
+  int probe[8];  // launch counters (diagnostics): insert, fsolve, fsweep, fsweep-final,
+                 // wait, sweep, sweep-final, server-chain
 };
 // the words the host loop polls, mirrored into mapped pinned memory
 struct SpecHost {
   volatile int conf, abort, abort_step, status, done;
+  volatile int seen[8];  // diagnostics: last step each kernel kind started (probe order)
 };
 struct SpecView {
   int n, cap, S, kind;
@@ -52,6 +55,7 @@ struct SpecView {
   double *rec_err, *rec_sec;
   SpecCtl* ctl;
   SpecHost* host;
+  unsigned long long watchdog_ns;
 };
 struct SpecStats {
   long long hits = 0, misses = 0, late = 0, rollbacks = 0;

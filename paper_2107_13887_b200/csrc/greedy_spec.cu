@@ -63,7 +63,7 @@ constexpr int kSweepT = 64;      // exact sweep CTA (one point per thread)
 constexpr int kSweepTile = 128;  // controls per smem tile
 constexpr int kFastT = 128;      // predictor sweep CTA
 constexpr int kFastTile = 256;
-constexpr unsigned long long kWatchdogNs = 60ull * 1000000000ull;
+
 
 __device__ __forceinline__ int4 ld_volatile4(const int* p) {
   int4 w;
@@ -174,6 +174,7 @@ template <int NR, int T>
 __global__ void __launch_bounds__(T) k_spec_insert(SpecView v, int k, int ep) {
   extern __shared__ double sh[];
   __shared__ int s_node, s_exact;
+  if (threadIdx.x == 0) atomicAdd(&v.ctl->probe[0], 1), v.host->seen[0] = k;
   if (!launch_live(v.ctl, ep)) return;
   if (threadIdx.x == 0) {
     int node = -1, exact = 0;
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(1024) k_fast_solve(SpecView v, int n, int ep) 
   __shared__ double sb[3][32], rc[32];
   __shared__ double T[32][33];  // T[t][r] = L_{b0+r, b0+t}
   __shared__ int s_ok;
+  if (threadIdx.x == 0) atomicAdd(&v.ctl->probe[1], 1), v.host->seen[1] = n;
   if (!launch_live(v.ctl, ep)) return;
   if (threadIdx.x == 0) s_ok = ld_volatile(&v.ins_ep[n - 1]) == ep;
   __syncthreads();
@@ -282,6 +284,7 @@ __global__ void __launch_bounds__(1024) k_fast_solve(SpecView v, int n, int ep) 
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     v.fax[i] = xs[i], v.fay[i] = xs[cap + i], v.faz[i] = xs[2 * cap + i];
+  if (threadIdx.x == 0) v.host->seen[1] = -n;  // diagnostics: finished
 }
 
 __device__ __forceinline__ double fast_wendland(int kind, double eta) {
@@ -333,6 +336,7 @@ __global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep
   __shared__ __align__(16) double ct[kFastTile][6];
   __shared__ Top2 wt[kFastT / 32];
   __shared__ bool last;
+  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&v.ctl->probe[2], 1), v.host->seen[2] = k;
   const bool live_blk = launch_live(v.ctl, ep);
   const int n = v.n;
   const int i = blockIdx.x * kFastT + threadIdx.x;
@@ -387,6 +391,7 @@ __global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep
     r = merge2(r, Top2{((volatile double*)v.fbv)[b], ((volatile double*)v.fbv2)[b],
                        ((volatile int*)v.fbi)[b]});
   v.pred_gap[k] = r.v1 > 0.0 ? (r.v1 - fmax(r.v2, 0.0)) / r.v1 : -1.0;
+  atomicAdd(&v.ctl->probe[3], 1), v.host->seen[3] = k;
   __threadfence();
   v.pred_node[k] = (r.v1 >= 0.0 && r.i1 < n) ? r.i1 : -1;
 }
@@ -395,12 +400,13 @@ __global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep
 // exact sweep(k): greedy.cpp:122-153 with alpha_k from its slot
 // ---------------------------------------------------------------------------
 __global__ void k_spec_wait_chain(SpecView v, int k, int ep) {
+  atomicAdd(&v.ctl->probe[4], 1), v.host->seen[4] = k;
   const unsigned long long t0 = globaltimer();
   for (;;) {
     const int4 w = ld_volatile4(&v.ctl->epoch);
     if (w.x != ep || w.y != 0 || w.w != 0) return;
     if (ld_volatile(&v.chain_ep[k]) == ep) return;
-    if (globaltimer() - t0 > kWatchdogNs) {
+    if (globaltimer() - t0 > v.watchdog_ns) {
       finish(v, kStatusWatchdog, k);
       return;
     }
@@ -414,6 +420,7 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
   __shared__ double wv[kSweepT / 32], wa[kSweepT / 32], wv2[kSweepT / 32];
   __shared__ int wi[kSweepT / 32];
   __shared__ bool last;
+  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&v.ctl->probe[5], 1), v.host->seen[5] = k;
   const bool live_blk = launch_live(v.ctl, ep);  // see k_fast_sweep on the ticket
   const int n = v.n;
   const int slot = k % v.S;
@@ -507,6 +514,7 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
     if (w.x != ep || w.y != 0 || w.w != 0) return;
   }
   const double achieved = v.target_max > 0.0 ? exact::div(ov, v.target_max) : 0.0;
+  atomicAdd(&c->probe[6], 1), v.host->seen[6] = k;
   v.rec_err[k - 1] = achieved;
   v.rec_sec[k - 1] = (double)(globaltimer() - c->t0) * 1e-9;
   v.exact_gap[k] = r.v1 > 0.0 ? (r.v1 - fmax(r.v2, 0.0)) / r.v1 : -1.0;
@@ -599,7 +607,7 @@ __global__ void __launch_bounds__(64) k_chain_server(SpecView v) {
           s_ep = w.x;
           break;
         }
-        if (globaltimer() - t0 > kWatchdogNs) {
+        if (globaltimer() - t0 > v.watchdog_ns) {
           finish(v, kStatusWatchdog, k);
           break;
         }
@@ -610,6 +618,7 @@ __global__ void __launch_bounds__(64) k_chain_server(SpecView v) {
     __syncthreads();
     if (!s_go) return;
     const int kk = s_k, ep = s_ep;
+    if (threadIdx.x == 0) atomicAdd(&v.ctl->probe[7], 1), v.host->seen[7] = kk;
     double* out = v.slots + (size_t)(kk % S) * 3 * v.cap;
     gdev::ChainIO io{v.Lt, (size_t)v.cap, v.diag, v.yx, v.yy, v.yz, out, out + v.cap,
                      out + 2 * v.cap, XS_SMEM ? nullptr : v.xs_global + (size_t)j * 4 * v.cap};
@@ -659,6 +668,8 @@ SpecView GreedyEngine::spec_view() {
   s.rec_err = rec_err_.p, s.rec_sec = rec_sec_.p;
   s.ctl = sp_ctl_.p;
   s.host = sp_host_dev_;
+  const char* we = std::getenv("IMB_SPEC_WATCHDOG_S");
+  s.watchdog_ns = (unsigned long long)((we ? std::atof(we) : 60.0) * 1e9);
   return s;
 }
 
@@ -695,8 +706,25 @@ void GreedyEngine::spec_alloc() {
   for (auto kern : {k_spec_insert<4, 1024>, k_spec_insert<2, 1024>})
     IMB_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(ins_smem_, 48 * 1024)));
+  // Load every kernel of the pipeline now: under lazy module loading (the
+  // CUDA 12 default) a kernel's first launch loads its code, which waits for
+  // the device -- and the device never idles while the chain server spins.
+  {
+    cudaFuncAttributes fa;
+    const void* fns[] = {
+        (const void*)k_spec_init,         (const void*)k_spec_rollback,
+        (const void*)k_spec_insert<4, 1024>, (const void*)k_spec_insert<2, 1024>,
+        (const void*)k_fast_solve,        (const void*)k_fast_sweep,
+        (const void*)k_spec_wait_chain,   (const void*)k_spec_sweep<-1>,
+        (const void*)k_spec_sweep<C0>,    (const void*)k_spec_sweep<C2>,
+        (const void*)k_spec_sweep<C4>,    (const void*)k_spec_sweep<C6>,
+        (const void*)k_chain_server<true>, (const void*)k_chain_server<false>};
+    for (const void* f : fns) IMB_CHECK(cudaFuncGetAttributes(&fa, f));
+  }
   int lo, hi;
   IMB_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  const char* pe = std::getenv("IMB_SPEC_PRIO");
+  if (pe && pe[0] == '0') hi = lo;
   IMB_CHECK(cudaStreamCreateWithPriority(&sp_pred_, cudaStreamNonBlocking, hi));
   IMB_CHECK(cudaStreamCreateWithPriority(&sp_chain_, cudaStreamNonBlocking, lo));
   sp_ready_ = true;
@@ -774,6 +802,15 @@ const GState& GreedyEngine::run_level_spec() {
       next = r + 1;
       continue;
     }
+    if (std::getenv("IMB_SPEC_TRACE")) {
+      static auto last = std::chrono::steady_clock::now();
+      if (std::chrono::steady_clock::now() - last > std::chrono::seconds(3)) {
+        last = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[spec] host next=%d conf=%d seen ins %d fsolve %d fsweep %d/%d wait %d sweep %d/%d chain %d\n",
+                     next, h->conf, h->seen[0], h->seen[1], h->seen[2], h->seen[3], h->seen[4],
+                     h->seen[5], h->seen[6], h->seen[7]);
+      }
+    }
     if (std::chrono::steady_clock::now() - t_start > std::chrono::seconds(3600))
       throw std::runtime_error("speculative greedy: host watchdog");
     std::this_thread::yield();
@@ -795,6 +832,9 @@ const GState& GreedyEngine::run_level_spec() {
                  "final=%d hits=%d misses=%d late=%d rollbacks=%d\n",
                  c.epoch, c.abort, c.abort_step, c.done, c.rb_step, c.conf, c.final_step, c.hits,
                  c.misses, c.late, c.rollbacks);
+    std::fprintf(stderr, "[spec] probes: insert %d fsolve %d fsweep %d/%d wait %d sweep %d/%d chains %d\n",
+                 c.probe[0], c.probe[1], c.probe[2], c.probe[3], c.probe[4], c.probe[5], c.probe[6],
+                 c.probe[7]);
     for (int k = std::max(0, c.conf - 2); k <= std::min(cap_, c.conf + 6); ++k)
       std::fprintf(stderr, "[spec]  k=%d state=%x ins_ep=%d chain_ep=%d ins_node=%d ins_fail=%d pred=%d\n",
                    k, w[k], w[m + k], w[2 * m + k], w[3 * m + k], w[4 * m + k], w[5 * m + k]);
