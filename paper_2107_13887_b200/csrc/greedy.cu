@@ -45,7 +45,6 @@ namespace imb {
 namespace {
 
 constexpr int kInsertThreads = 1024;
-constexpr int kMaxCap = 8192;  // k_insert: rr + ring[2] in shared memory
 constexpr int kSweepThreads = 64;
 constexpr int kSweepTile = 128;
 
@@ -66,11 +65,12 @@ __global__ void __launch_bounds__(T) k_insert(GView g) {
   const int node = st.next;
   if (k == 0 && threadIdx.x == 0) st.t0 = globaltimer();
   gdev::InsertIO io{g.px, g.py, g.pz, g.tx, g.ty, g.tz, g.cx, g.cy, g.cz, g.Lt, (size_t)g.cap,
-                    g.diag, g.yx, g.yy, g.yz, g.kind, g.R};
-  bool ok;
-  const double pivot = gdev::insert_row<NR, T>(io, k, node, st.max_diag, sh, &ok);
+                    g.diag, g.yx, g.yy, g.yz, g.kind, g.R, g.rr_global};
+  const gdev::AppendOut a = gdev::insert_row<NR, T>(io, k, node, nullptr, st.max_diag, sh);
+  const bool ok = a.ok;
+  const double pivot = a.pivot;
   if (threadIdx.x == 0) {
-    st.max_diag = (st.max_diag < 1.0) ? 1.0 : st.max_diag;
+    st.max_diag = a.max_diag;
     if (!ok) {
       st.status = kStatusSolveError;
       st.fail_node = node;
@@ -225,9 +225,6 @@ __global__ void k_next_in_order(GView g, int n) {
 // host side
 // ---------------------------------------------------------------------------
 GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap_(cap) {
-  if (cap > kMaxCap)
-    throw InvalidArgument("max_points_per_level above " + std::to_string(kMaxCap) +
-                          " is not supported by this build");
   pos_.reserve(n);
   tgt_.reserve(n);
   res_.reserve(n);
@@ -262,10 +259,16 @@ GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap
                                    (int)std::max<size_t>(bw_smem_, 48 * 1024)));
   // k_insert: rr + ring[2] (+ dg staging, which also makes room for y)
   // k_insert: rr + a ring of 4 columns when it fits (cap <= 5812), else 2
-  ins_ring_ = (size_t)cap * 8 * 5 <= 227 * 1024 && !std::getenv("IMB_INSERT_RING2") ? 4 : 2;
-  ins_smem_ = (size_t)cap * 8 * (1 + ins_ring_);
+  // k_insert: rr + a ring of 4 columns when it fits (cap <= 5785), else 2
+  // (cap <= 9642), else rr in global memory and L read directly
+  const size_t smem_max = 226 * 1024;
+  ins_ring_ = (size_t)cap * 8 * 5 <= smem_max && !std::getenv("IMB_INSERT_RING2") ? 4
+              : (size_t)cap * 8 * 3 <= smem_max                                  ? 2
+                                                                                  : 0;
+  ins_smem_ = ins_ring_ ? (size_t)cap * 8 * (1 + ins_ring_) : 0;
+  if (!ins_ring_) rr_.reserve(cap);
   if (const char* e = std::getenv("IMB_INSERT_T")) ins_threads_ = std::atoi(e);
-  for (auto kern : {k_insert<4>, k_insert<4, 256>, k_insert<4, 512>, k_insert<2>})
+  for (auto kern : {k_insert<4>, k_insert<4, 256>, k_insert<4, 512>, k_insert<2>, k_insert<0>})
     IMB_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(ins_smem_, 48 * 1024)));
 }
@@ -293,6 +296,7 @@ GView GreedyEngine::view() {
   g.yx = y_.x.p, g.yy = y_.y.p, g.yz = y_.z.p;
   g.ax = alpha_.x.p, g.ay = alpha_.y.p, g.az = alpha_.z.p;
   g.xs_global = xs_.p;
+  g.rr_global = rr_.p;
   g.bv = bv_.p, g.ba = ba_.p, g.bi = bi_.p;
   g.rec_err = rec_err_.p;
   g.rec_sec = rec_sec_.p;
@@ -362,8 +366,10 @@ void GreedyEngine::launch_insert(const GView& g) {
     k_insert<4, 512><<<1, 512, ins_smem_, ctx_.stream>>>(g);
   else if (ins_ring_ == 4)
     k_insert<4><<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);
-  else
+  else if (ins_ring_ == 2)
     k_insert<2><<<1, kInsertThreads, ins_smem_, ctx_.stream>>>(g);
+  else
+    k_insert<0><<<1, kInsertThreads, 0, ctx_.stream>>>(g);
 }
 
 void GreedyEngine::enqueue_step(bool sweep) {
@@ -387,7 +393,7 @@ void GreedyEngine::enqueue_step(bool sweep) {
 const GState& GreedyEngine::run_level(int batch) {
   // the speculative pipeline (greedy_spec.cu) unless IMB_SPEC=0
   const char* e = std::getenv("IMB_SPEC");
-  if (!(e && e[0] == '0')) return run_level_spec();
+  if (!(e && e[0] == '0') && (size_t)cap_ * 24 <= 200 * 1024) return run_level_spec();
   for (;;) {
     for (int b = 0; b < batch; ++b) enqueue_step(true);
     const GState& s = poll();

@@ -44,12 +44,14 @@ struct SpecView {
   double *yx, *yy, *yz;
   double* slots;      // [S][3][cap] alpha of step k in slot k % S
   double* xs_global;  // [S][4][cap] chain workspace when smem is too small
+  double* rr_global;  // [cap] insert scratch when smem is too small
   double *fax, *fay, *faz;  // predictor alpha
   int* selstep;       // [n] step at which the node was inserted (INT_MAX: not)
   int *state, *ins_ep, *chain_ep, *ins_node, *ins_fail, *pred_node;  // [cap + 1]
+  int *pred2_node, *exact_node;                                      // [cap + 1]
   double *pivot, *pred_gap, *exact_gap;                              // [cap + 1]
   double *bv, *bv2, *ba;
-  int* bi;
+  int *bi, *bi2;
   double *fbv, *fbv2;
   int* fbi;
   double *rec_err, *rec_sec;
@@ -89,6 +91,7 @@ struct GView {
   double *yx, *yy, *yz;        // forward solutions
   double *ax, *ay, *az;        // alpha
   double* xs_global;           // backward-chain workspace when smem is too small
+  double* rr_global;           // k_insert row scratch when smem is too small
   double *bv, *ba;
   int* bi;
   double *rec_err, *rec_sec;
@@ -145,7 +148,7 @@ class GreedyEngine {
   DPoints pos_, tgt_, res_, cpos_, y_, alpha_;
   DBuf<unsigned char> sel_;
   DBuf<int> cidx_;
-  DBuf<double> lt_, xs_, bv_, ba_, rec_err_, rec_sec_;
+  DBuf<double> lt_, xs_, rr_, bv_, ba_, rec_err_, rec_sec_;
   DBuf<double2> diag_;
   DBuf<int> bi_;
   DBuf<GState> st_;
@@ -156,7 +159,7 @@ class GreedyEngine {
   int spec_S_ = 32, sp_fnblk_ = 1;
   size_t sp_server_smem_ = 0, sp_fsolve_smem_ = 0;
   DBuf<double> sp_slots_, sp_fa_, sp_xs_, sp_dwords_, sp_bv2_, sp_fbv_;
-  DBuf<int> sp_selstep_, sp_words_, sp_fbi_;
+  DBuf<int> sp_selstep_, sp_words_, sp_fbi_, sp_bi2_;
   DBuf<SpecCtl> sp_ctl_;
   SpecHost* sp_host_ = nullptr;
   SpecHost* sp_host_dev_ = nullptr;

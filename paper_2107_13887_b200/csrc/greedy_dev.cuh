@@ -81,19 +81,74 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 // ---------------------------------------------------------------------------
-// Row append: greedy.cpp:86-112 / rbf.cpp:71-100
+// Forward substitution and row append: rbf.cpp:71-100 / rbf.cpp:107-112
 //
-// Shared memory: rr[cap] (running s_j, then row[j]) | ring[NR][cap] (columns
-// m .. m+NR-1 of L, streamed by cp.async NR-1 steps ahead: every thread
-// copies exactly the rows it owns, so cp.async.wait_group alone orders the
-// copy before its own use and no barrier guards the ring).  The pivot pair
-// (L_mm, 1/L_mm) of row m is held in a register by m's owner thread, loaded
-// T steps ahead.  Per step the critical path is the owner's division, one
-// barrier and the next owner's mul-sub.
+// forward_subst solves L s = b for the first k rows, right-looking: once
+// s_m is final (s_m / L_mm), every s_j (j > m) does s_j -= L_jm * s_m, so
+// each s_j receives its subtractions in ascending m exactly as in the
+// reference's inner loops (rbf.cpp:84, rbf.cpp:110).  Shared memory (NR >= 2):
+// rr[cap] (running s_j) | ring[NR][cap] (columns m .. m+NR-1 of L, streamed
+// by cp.async NR-1 steps ahead: every thread copies exactly the rows it
+// owns, so cp.async.wait_group alone orders the copy before its own use and
+// no barrier guards the ring).  NR == 0 (factors too large for shared
+// memory): rr in global memory, L read directly.  The pivot pair (L_mm,
+// 1/L_mm) of row m is held in a register by m's owner thread, loaded T steps
+// ahead.  Per step the critical path is the owner's division, one barrier
+// and the next owner's mul-sub.
 // ---------------------------------------------------------------------------
+template <int NR, int T>
+__device__ void forward_subst(const double* Lt, const double2* diag, size_t cap, int k, double* rr,
+                              double* ring) {
+  const int tid = threadIdx.x;
+  double2 dm = tid < k ? diag[tid] : make_double2(1.0, 1.0);  // pivot of my next row
+  int mi = 0, ji = tid > 0 ? tid : T;  // next column to issue, my first row > mi
+  const double* ci = Lt;               // its start, colstart(mi, cap)
+  auto issue_next = [&]() {
+    if (NR > 0) {
+      if (mi < k) {
+        double* dst = ring + (mi & (NR - 1)) * cap;
+        for (int j = ji; j < k; j += T) cp_async8(dst + j, ci + (j - mi));
+      }
+      cp_async_commit();
+    }
+    ci += cap - (size_t)mi;  // colstart(mi + 1) = colstart(mi) + cap - mi
+    ++mi;
+    if (ji == mi) ji += T;
+  };
+  if (NR > 0) {
+#pragma unroll
+    for (int q = 0; q < NR - 1; ++q) issue_next();
+  }
+  __syncthreads();
+  int ju = tid > 0 ? tid : T;  // my first row > m
+  const double* cm = Lt;       // colstart(m, cap) (NR == 0)
+  for (int m = 0; m < k; ++m) {
+    if ((m & (T - 1)) == tid) {
+      rr[m] = exact::div_rcp(rr[m], exact::Recip{dm.x, dm.y});  // s / L_mm
+      if (m + T < k) dm = diag[m + T];
+    }
+    if (NR > 0) {
+      issue_next();             // column m + NR - 1
+      cp_async_wait<NR - 1>();  // my copies of column m have landed
+    }
+    __syncthreads();
+    const double r = rr[m];
+    if (NR > 0) {
+      const double* lc = ring + (m & (NR - 1)) * cap;
+      for (int j = ju; j < k; j += T) rr[j] = exact::sub(rr[j], exact::mul(lc[j], r));
+    } else {
+      for (int j = ju; j < k; j += T) rr[j] = exact::sub(rr[j], exact::mul(cm[j - m], r));
+      cm += cap - (size_t)m;
+    }
+    if (ju == m + 1) ju += T;
+  }
+  if (NR > 0) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+}
+
 struct InsertIO {
-  const double *px, *py, *pz;  // surface positions
-  const double *tx, *ty, *tz;  // level target (rhs = target[c_k], greedy.cpp:104)
+  const double *px, *py, *pz;  // surface positions (greedy) -- unused with col_in
+  const double *tx, *ty, *tz;  // level target (rhs = target[c_k], greedy.cpp:104); null: no y
   const double *cx, *cy, *cz;  // control positions c_0..c_{k-1} (insertion order)
   double* Lt;
   size_t cap;
@@ -101,66 +156,46 @@ struct InsertIO {
   double *yx, *yy, *yz;        // forward solutions y_0..y_{k-1} in, y_k out
   int kind;
   double R;
+  double* rr_global;           // [cap] scratch when NR == 0
 };
 
-// Appends row k for surface node `node`.  Returns the pivot; on success
-// (pivot > 1e-14 * max_diag, rbf.cpp:92) writes diag[k], L_kk, the row
-// L_k0..L_k,k-1 into the columns and y_k.  On failure writes nothing to L.
-// Every thread returns the same value; *ok is the success flag.
+struct AppendOut {
+  double pivot, max_diag;
+  bool ok;
+};
+
+// Appends row k (rbf.cpp:71-100).  The new column is col_in[0..k] when given
+// (CholeskyFactor::append), else phi(|c_m - p_node|) with diagonal 1.0
+// (greedy.cpp:87-93).  max_diag is the factor's running maximum diagonal,
+// updated before the pivot test as in rbf.cpp:89.  On success (pivot >
+// 1e-14 * max_diag, rbf.cpp:92) writes diag[k], L_kk, the row L_k0..L_k,k-1
+// into the columns and, when the target is given, y_k.  On failure writes
+// nothing to L.  Every thread returns the same value.
 template <int NR, int T>
-__device__ double insert_row(const InsertIO& g, int k, int node, double max_diag, double* sh,
-                             bool* ok) {
-  __shared__ double s_pivot;
+__device__ AppendOut insert_row(const InsertIO& g, int k, int node, const double* col_in,
+                                double max_diag, double* sh) {
+  __shared__ double s_pivot, s_maxd;
   __shared__ int s_ok;
   const size_t cap = g.cap;
-  double* rr = sh;          // [cap]
-  double* ring = sh + cap;  // [NR][cap]
+  double* rr = NR > 0 ? sh : g.rr_global;  // [cap]
+  double* ring = sh + cap;                 // [NR][cap]
   const int tid = threadIdx.x;
-
-  const double px = g.px[node], py = g.py[node], pz = g.pz[node];
-  const exact::Recip rR = exact::make_recip(g.R);
-  double2 dm = tid < k ? g.diag[tid] : make_double2(1.0, 1.0);  // pivot of my next row
-  // column (greedy.cpp:87-93 / rbf.cpp:167-170): phi(distance(c_m, p_new))
-  for (int j = tid; j < k; j += T) {
-    const double d = exact::dist(g.cx[j], g.cy[j], g.cz[j], px, py, pz);
-    rr[j] = exact::wendland_rt(g.kind, exact::div_rcp(d, rR));
-  }
-  // Right-looking forward substitution (rbf.cpp:80-87): once row[m] is final,
-  // every s_j (j > m) does s_j -= L_jm * row[m], so each s_j receives its
-  // subtractions in ascending m exactly as in the reference's inner loop.
-  int mi = 0, ji = tid > 0 ? tid : T;  // next column to issue, my first row > mi
-  const double* ci = g.Lt;             // its start, colstart(mi, cap)
-  auto issue_next = [&]() {
-    if (mi < k) {
-      double* dst = ring + (mi & (NR - 1)) * cap;
-      for (int j = ji; j < k; j += T) cp_async8(dst + j, ci + (j - mi));
+  if (col_in) {
+    for (int j = tid; j < k; j += T) rr[j] = col_in[j];
+  } else {
+    // column (greedy.cpp:87-93 / rbf.cpp:167-170): phi(distance(c_m, p_new))
+    const double px = g.px[node], py = g.py[node], pz = g.pz[node];
+    const exact::Recip rR = exact::make_recip(g.R);
+    for (int j = tid; j < k; j += T) {
+      const double d = exact::dist(g.cx[j], g.cy[j], g.cz[j], px, py, pz);
+      rr[j] = exact::wendland_rt(g.kind, exact::div_rcp(d, rR));
     }
-    cp_async_commit();
-    ci += cap - (size_t)mi;  // colstart(mi + 1) = colstart(mi) + cap - mi
-    ++mi;
-    if (ji == mi) ji += T;
-  };
-#pragma unroll
-  for (int q = 0; q < NR - 1; ++q) issue_next();
-  __syncthreads();
-  int ju = tid > 0 ? tid : T;  // my first row > m
-  for (int m = 0; m < k; ++m) {
-    if ((m & (T - 1)) == tid) {
-      rr[m] = exact::div_rcp(rr[m], exact::Recip{dm.x, dm.y});  // row[j] = s / lj[j]
-      if (m + T < k) dm = g.diag[m + T];
-    }
-    issue_next();             // column m + NR - 1
-    cp_async_wait<NR - 1>();  // my copies of column m have landed
-    __syncthreads();
-    const double r = rr[m];
-    const double* lc = ring + (m & (NR - 1)) * cap;
-    for (int j = ju; j < k; j += T) rr[j] = exact::sub(rr[j], exact::mul(lc[j], r));
-    if (ju == m + 1) ju += T;
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  forward_subst<NR, T>(g.Lt, g.diag, cap, k, rr, ring);
   // stage y_0..y_{k-1} for the forward chain in the ring space when it fits
+  const bool with_y = g.tx != nullptr;
   const double *yxs = g.yx, *yys = g.yy, *yzs = g.yz;
-  if (NR >= 3) {
+  if (NR >= 3 && with_y) {
     double* ys = sh + cap;
     for (int j = tid; j < k; j += T)
       ys[j] = g.yx[j], ys[cap + j] = g.yy[j], ys[2 * cap + j] = g.yz[j];
@@ -171,36 +206,44 @@ __device__ double insert_row(const InsertIO& g, int k, int node, double max_diag
   // i = k), both sequential chains; 4 independent chains interleaved.
   if (tid == 0) {
     double sq = 0.0;
-    double yx = g.tx[node], yy = g.ty[node], yz = g.tz[node];  // rhs_k = target[c_k]
+    double yx = 0.0, yy = 0.0, yz = 0.0;
+    if (with_y) {
+      yx = g.tx[node], yy = g.ty[node], yz = g.tz[node];  // rhs_k = target[c_k]
 #pragma unroll 8
-    for (int j = 0; j < k; ++j) {
-      const double r = rr[j];
-      sq = exact::add(sq, exact::mul(r, r));
-      yx = exact::sub(yx, exact::mul(r, yxs[j]));
-      yy = exact::sub(yy, exact::mul(r, yys[j]));
-      yz = exact::sub(yz, exact::mul(r, yzs[j]));
+      for (int j = 0; j < k; ++j) {
+        const double r = rr[j];
+        sq = exact::add(sq, exact::mul(r, r));
+        yx = exact::sub(yx, exact::mul(r, yxs[j]));
+        yy = exact::sub(yy, exact::mul(r, yys[j]));
+        yz = exact::sub(yz, exact::mul(r, yzs[j]));
+      }
+    } else {
+#pragma unroll 8
+      for (int j = 0; j < k; ++j) sq = exact::add(sq, exact::mul(rr[j], rr[j]));
     }
-    const double diag = 1.0;  // column[k] = 1.0 (greedy.cpp:93, rbf.cpp:171)
-    max_diag = (max_diag < diag) ? diag : max_diag;
+    const double diag = col_in ? col_in[k] : 1.0;  // column[k] (greedy.cpp:93, rbf.cpp:88)
+    max_diag = (max_diag < diag) ? diag : max_diag;  // std::max (rbf.cpp:89)
     const double pivot_sq = exact::sub(diag, sq);
     const double pivot = pivot_sq > 0.0 ? __dsqrt_rn(pivot_sq) : 0.0;
     s_pivot = pivot;
+    s_maxd = max_diag;
     s_ok = pivot > exact::mul(1e-14, max_diag);
     if (s_ok) {
       const exact::Recip pr = exact::make_recip(pivot);
       g.diag[k] = make_double2(pivot, pr.y);
       g.Lt[colstart(k, cap)] = pivot;
-      g.yx[k] = exact::div_rcp(yx, pr);
-      g.yy[k] = exact::div_rcp(yy, pr);
-      g.yz[k] = exact::div_rcp(yz, pr);
+      if (with_y) {
+        g.yx[k] = exact::div_rcp(yx, pr);
+        g.yy[k] = exact::div_rcp(yy, pr);
+        g.yz[k] = exact::div_rcp(yz, pr);
+      }
     }
   }
   __syncthreads();
-  const double pivot = s_pivot;
-  *ok = s_ok != 0;
-  if (*ok)  // scatter the new row into the columns: L_kj at column j, offset k - j
+  AppendOut out{s_pivot, s_maxd, s_ok != 0};
+  if (out.ok)  // scatter the new row into the columns: L_kj at column j, offset k - j
     for (int j = tid; j < k; j += T) g.Lt[colstart(j, cap) + (k - j)] = rr[j];
-  return pivot;
+  return out;
 }
 
 // ---------------------------------------------------------------------------

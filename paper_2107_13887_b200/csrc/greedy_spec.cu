@@ -120,7 +120,7 @@ __global__ void k_spec_init(SpecView v) {
   for (int k = t; k <= v.cap; k += stride) {
     v.state[k] = k == 0 ? (0 | kExactBit) : kEmpty;  // c_0 = surface node 0 (greedy.cpp:115)
     v.ins_ep[k] = -1, v.chain_ep[k] = -1, v.ins_node[k] = -1, v.ins_fail[k] = 0;
-    v.pred_node[k] = -1;
+    v.pred_node[k] = -1, v.pred2_node[k] = -1, v.exact_node[k] = -1;
     v.pred_gap[k] = -1.0, v.exact_gap[k] = -1.0;
   }
   if (t == 0) {
@@ -199,9 +199,10 @@ __global__ void __launch_bounds__(T) k_spec_insert(SpecView v, int k, int ep) {
   const int node = s_node;
   if (node < 0) return;  // no prediction (no candidate left): sweep(k) decides
   gdev::InsertIO io{v.px, v.py, v.pz, v.tx, v.ty, v.tz, v.cx, v.cy, v.cz, v.Lt, (size_t)v.cap,
-                    v.diag, v.yx, v.yy, v.yz, v.kind, v.R};
-  bool ok;
-  const double pivot = gdev::insert_row<NR, T>(io, k, node, 1.0, sh, &ok);
+                    v.diag, v.yx, v.yy, v.yz, v.kind, v.R, v.rr_global};
+  const gdev::AppendOut a = gdev::insert_row<NR, T>(io, k, node, nullptr, 1.0, sh);
+  const bool ok = a.ok;
+  const double pivot = a.pivot;
   if (threadIdx.x == 0) {
     v.ins_node[k] = node;
     v.pivot[k] = pivot;
@@ -302,14 +303,20 @@ __device__ __forceinline__ double fast_wendland(int kind, double eta) {
 
 struct Top2 {
   double v1, v2;
-  int i1;
+  int i1, i2;
 };
+// the two best (value, index) pairs, lowest index on ties
+__device__ __forceinline__ bool beats(double v, int i, double w, int j) {
+  return v > w || (v == w && i < j);
+}
 __device__ __forceinline__ Top2 merge2(Top2 a, Top2 b) {
   Top2 r;
-  if (b.v1 > a.v1 || (b.v1 == a.v1 && b.i1 < a.i1)) {
-    r.v1 = b.v1, r.i1 = b.i1, r.v2 = fmax(a.v1, b.v2);
+  if (beats(b.v1, b.i1, a.v1, a.i1)) {
+    r.v1 = b.v1, r.i1 = b.i1;
+    if (beats(a.v1, a.i1, b.v2, b.i2)) r.v2 = a.v1, r.i2 = a.i1; else r.v2 = b.v2, r.i2 = b.i2;
   } else {
-    r.v1 = a.v1, r.i1 = a.i1, r.v2 = fmax(a.v2, b.v1);
+    r.v1 = a.v1, r.i1 = a.i1;
+    if (beats(b.v1, b.i1, a.v2, a.i2)) r.v2 = b.v1, r.i2 = b.i1; else r.v2 = a.v2, r.i2 = a.i2;
   }
   return r;
 }
@@ -319,6 +326,7 @@ __device__ __forceinline__ Top2 warp_top2(Top2 t) {
     u.v1 = __shfl_xor_sync(0xffffffffu, t.v1, o);
     u.v2 = __shfl_xor_sync(0xffffffffu, t.v2, o);
     u.i1 = __shfl_xor_sync(0xffffffffu, t.i1, o);
+    u.i2 = __shfl_xor_sync(0xffffffffu, t.i2, o);
     t = merge2(t, u);
   }
   return t;
@@ -362,7 +370,7 @@ __global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep
       }
     }
   }
-  Top2 t{-1.0, -1.0, n};
+  Top2 t{-1.0, -1.0, n, n};
   if (live && v.selstep[i] >= k) {
     const double ex = v.tx[i] - fx, ey = v.ty[i] - fy, ez = v.tz[i] - fz;
     const double q = fma(ex, ex, fma(ey, ey, ez * ez));
@@ -375,6 +383,7 @@ __global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep
   if (threadIdx.x == 0) {
     for (int w = 1; w < kFastT / 32; ++w) t = merge2(t, wt[w]);
     v.fbv[blockIdx.x] = t.v1, v.fbv2[blockIdx.x] = t.v2, v.fbi[blockIdx.x] = t.i1;
+    v.fbi[gridDim.x + blockIdx.x] = t.i2;
     __threadfence();
     last = atomicAdd(&v.ctl->fticket, 1) == (int)gridDim.x - 1;
   }
@@ -386,10 +395,11 @@ __global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep
     const int4 w = ld_volatile4(&v.ctl->epoch);
     if (w.x != ep || w.y != 0 || w.w != 0) return;
   }
-  Top2 r{-1.0, -1.0, n};
+  Top2 r{-1.0, -1.0, n, n};
   for (int b = 0; b < (int)gridDim.x; ++b)
     r = merge2(r, Top2{((volatile double*)v.fbv)[b], ((volatile double*)v.fbv2)[b],
-                       ((volatile int*)v.fbi)[b]});
+                       ((volatile int*)v.fbi)[b], ((volatile int*)v.fbi)[gridDim.x + b]});
+  v.pred2_node[k] = r.v2 >= 0.0 && r.i2 < n ? r.i2 : -1;
   v.pred_gap[k] = r.v1 > 0.0 ? (r.v1 - fmax(r.v2, 0.0)) / r.v1 : -1.0;
   atomicAdd(&v.ctl->probe[3], 1), v.host->seen[3] = k;
   __threadfence();
@@ -418,7 +428,7 @@ template <int KIND>
 __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int ep) {
   __shared__ __align__(16) double ct[kSweepTile][6];
   __shared__ double wv[kSweepT / 32], wa[kSweepT / 32], wv2[kSweepT / 32];
-  __shared__ int wi[kSweepT / 32];
+  __shared__ int wi[kSweepT / 32], wi2[kSweepT / 32];
   __shared__ bool last;
   if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&v.ctl->probe[5], 1), v.host->seen[5] = k;
   const bool live_blk = launch_live(v.ctl, ep);  // see k_fast_sweep on the ticket
@@ -462,7 +472,7 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
     }
   }
   double nv = -1.0, all = 0.0, nv2 = -1.0;
-  int ni = n;
+  int ni = n, ni2 = n;
   if (live && live_blk) {
     const double ex = exact::sub(v.tx[i], fx), ey = exact::sub(v.ty[i], fy),
                  ez = exact::sub(v.tz[i], fz);
@@ -475,22 +485,24 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
     const double v2 = __shfl_xor_sync(0xffffffffu, nv, o);
     const double s2 = __shfl_xor_sync(0xffffffffu, nv2, o);
     const int i2 = __shfl_xor_sync(0xffffffffu, ni, o);
-    Top2 a{nv, nv2, ni};
-    a = merge2(a, Top2{v2, s2, i2});
-    nv = a.v1, nv2 = a.v2, ni = a.i1;
+    const int j2 = __shfl_xor_sync(0xffffffffu, ni2, o);
+    Top2 a{nv, nv2, ni, ni2};
+    a = merge2(a, Top2{v2, s2, i2, j2});
+    nv = a.v1, nv2 = a.v2, ni = a.i1, ni2 = a.i2;
     const double a2 = __shfl_xor_sync(0xffffffffu, all, o);
     all = (all < a2) ? a2 : all;
   }
   const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) wv[w] = nv, wi[w] = ni, wa[w] = all, wv2[w] = nv2;
+  if ((threadIdx.x & 31) == 0) wv[w] = nv, wi[w] = ni, wa[w] = all, wv2[w] = nv2, wi2[w] = ni2;
   __syncthreads();
   if (threadIdx.x == 0) {
-    Top2 a{nv, nv2, ni};
+    Top2 a{nv, nv2, ni, ni2};
     for (int t = 1; t < kSweepT / 32; ++t) {
-      a = merge2(a, Top2{wv[t], wv2[t], wi[t]});
+      a = merge2(a, Top2{wv[t], wv2[t], wi[t], wi2[t]});
       all = (all < wa[t]) ? wa[t] : all;
     }
     v.bv[blockIdx.x] = a.v1, v.bv2[blockIdx.x] = a.v2, v.bi[blockIdx.x] = a.i1;
+    v.bi2[blockIdx.x] = a.i2;
     v.ba[blockIdx.x] = all;
     __threadfence();
     last = atomicAdd(&v.ctl->ticket, 1) == (int)gridDim.x - 1;
@@ -499,11 +511,11 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
   if (!last || threadIdx.x != 0) return;
   // final block: grid argmax + decision (greedy.cpp:136-152)
   __threadfence();
-  Top2 r{-1.0, -1.0, n};
+  Top2 r{-1.0, -1.0, n, n};
   double ov = 0.0;
   for (int b = 0; b < (int)gridDim.x; ++b) {
     r = merge2(r, Top2{((volatile double*)v.bv)[b], ((volatile double*)v.bv2)[b],
-                       ((volatile int*)v.bi)[b]});
+                       ((volatile int*)v.bi)[b], ((volatile int*)v.bi2)[b]});
     const double a = ((volatile double*)v.ba)[b];
     ov = (ov < a) ? a : ov;
   }
@@ -521,6 +533,7 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
   c->achieved = achieved;
   c->overall = ov;
   const int mi = r.i1;
+  v.exact_node[k] = mi;
   if (achieved < v.tol) {
     finish(v, kStatusConverged, k);
     return;
@@ -654,12 +667,15 @@ SpecView GreedyEngine::spec_view() {
   s.yx = y_.x.p, s.yy = y_.y.p, s.yz = y_.z.p;
   s.slots = sp_slots_.p;
   s.xs_global = sp_xs_.p;
+  s.rr_global = rr_.p;
   s.fax = sp_fa_.p, s.fay = sp_fa_.p + cap_, s.faz = sp_fa_.p + 2 * (size_t)cap_;
   s.selstep = sp_selstep_.p;
   int* w = sp_words_.p;
   const size_t m = (size_t)cap_ + 1;
   s.state = w, s.ins_ep = w + m, s.chain_ep = w + 2 * m, s.ins_node = w + 3 * m,
-  s.ins_fail = w + 4 * m, s.pred_node = w + 5 * m;
+  s.ins_fail = w + 4 * m, s.pred_node = w + 5 * m, s.pred2_node = w + 6 * m,
+  s.exact_node = w + 7 * m;
+  s.bi2 = sp_bi2_.p;
   double* d = sp_dwords_.p;
   s.pivot = d, s.pred_gap = d + m, s.exact_gap = d + 2 * m;
   s.bv = bv_.p, s.ba = ba_.p, s.bi = bi_.p;
@@ -682,12 +698,13 @@ void GreedyEngine::spec_alloc() {
   sp_slots_.reserve((size_t)spec_S_ * 3 * cap_);
   sp_fa_.reserve(3 * (size_t)cap_);
   sp_selstep_.reserve(n_);
-  sp_words_.reserve(6 * m);
+  sp_words_.reserve(8 * m);
+  sp_bi2_.reserve(nblk_);
   sp_dwords_.reserve(3 * m);
   sp_bv2_.reserve(nblk_);
   sp_fnblk_ = (n_ + 127) / 128;
   sp_fbv_.reserve(2 * (size_t)sp_fnblk_);
-  sp_fbi_.reserve(sp_fnblk_);
+  sp_fbi_.reserve(2 * (size_t)sp_fnblk_);
   sp_ctl_.reserve(1);
   IMB_CHECK(cudaHostAlloc(&sp_host_, sizeof(SpecHost), cudaHostAllocMapped));
   IMB_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sp_host_dev_), sp_host_, 0));
@@ -703,7 +720,7 @@ void GreedyEngine::spec_alloc() {
   sp_fsolve_smem_ = 3 * (size_t)cap_ * 8;
   IMB_CHECK(cudaFuncSetAttribute(k_fast_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)std::max<size_t>(sp_fsolve_smem_, 48 * 1024)));
-  for (auto kern : {k_spec_insert<4, 1024>, k_spec_insert<2, 1024>})
+  for (auto kern : {k_spec_insert<4, 1024>, k_spec_insert<2, 1024>, k_spec_insert<0, 1024>})
     IMB_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(ins_smem_, 48 * 1024)));
   // Load every kernel of the pipeline now: under lazy module loading (the
@@ -714,6 +731,7 @@ void GreedyEngine::spec_alloc() {
     const void* fns[] = {
         (const void*)k_spec_init,         (const void*)k_spec_rollback,
         (const void*)k_spec_insert<4, 1024>, (const void*)k_spec_insert<2, 1024>,
+        (const void*)k_spec_insert<0, 1024>,
         (const void*)k_fast_solve,        (const void*)k_fast_sweep,
         (const void*)k_spec_wait_chain,   (const void*)k_spec_sweep<-1>,
         (const void*)k_spec_sweep<C0>,    (const void*)k_spec_sweep<C2>,
@@ -756,8 +774,10 @@ const GState& GreedyEngine::run_level_spec() {
   auto launch_insert = [&](int k, int ep) {
     if (ins_ring_ == 4)
       k_spec_insert<4, 1024><<<1, 1024, ins_smem_, sp>>>(v, k, ep);
-    else
+    else if (ins_ring_ == 2)
       k_spec_insert<2, 1024><<<1, 1024, ins_smem_, sp>>>(v, k, ep);
+    else
+      k_spec_insert<0, 1024><<<1, 1024, 0, sp>>>(v, k, ep);
   };
   auto launch_sweep = [&](int k, int ep) {
     k_spec_wait_chain<<<1, 1, 0, sm>>>(v, k, ep);
@@ -869,7 +889,8 @@ const GState& GreedyEngine::run_level_spec() {
   if (std::getenv("IMB_SPEC_LOG")) {
     const size_t m = (size_t)cap_ + 1;
     std::vector<double> pg(m), eg(m);
-    std::vector<int> words(6 * m);
+    std::vector<int> words(8 * m);
+    IMB_CHECK(cudaMemcpy(words.data(), sp_words_.p, words.size() * 4, cudaMemcpyDeviceToHost));
     IMB_CHECK(cudaMemcpy(pg.data(), sp_dwords_.p + m, m * 8, cudaMemcpyDeviceToHost));
     IMB_CHECK(cudaMemcpy(eg.data(), sp_dwords_.p + 2 * m, m * 8, cudaMemcpyDeviceToHost));
     std::fprintf(stderr, "[spec] n=%d cap=%d S=%d steps=%d hits=%d misses=%d late=%d rollbacks=%d\n",
@@ -877,7 +898,11 @@ const GState& GreedyEngine::run_level_spec() {
     if (FILE* f = std::fopen(std::getenv("IMB_SPEC_LOG"), "a")) {
       std::fprintf(f, "# level n=%d cap=%d steps=%d hits=%d misses=%d late=%d rollbacks=%d\n", n_,
                    cap_, fs, c.hits, c.misses, c.late, c.rollbacks);
-      for (int k = 1; k <= fs; ++k) std::fprintf(f, "%d %.3e %.3e\n", k, pg[k], eg[k]);
+      // k, predictor gap, exact gap, node inserted at k (last epoch), predicted 1st / 2nd,
+      // exact choice
+      for (int k = 1; k <= fs; ++k)
+        std::fprintf(f, "%d %.3e %.3e %d %d %d %d\n", k, pg[k], eg[k], words[3 * m + k],
+                     words[5 * m + k], words[6 * m + k], words[7 * m + k]);
       std::fclose(f);
     }
   }

@@ -1,3 +1,3 @@
-export PYTHONUNBUFFERED=1 IMB_SPEC_WATCHDOG_S=20
-timeout 300 python tools/spec_check.py cfg1 cfg2l01 cfg3p cfg4p > gpurun_out/a.log 2>&1
-grep -v "^\[spec\]  k=" gpurun_out/a.log | tail -n 30
+export PYTHONUNBUFFERED=1
+SPEC_SEQ=0 timeout 900 python tools/spec_check.py cfg4l01 cfg2 > gpurun_out/spec_big.log 2>&1
+cat gpurun_out/spec_big.log
