@@ -20,9 +20,10 @@
  * SPEC.md:350).  A context must not be used by two threads at once.
  *
  * Precision (additive extension):
- *   IM_EXACT   reference arithmetic order, bit-identical results
- *   IM_FP64    FMA fast path, <= 1e-10 relative to the reference (default
- *              for the volume update)
+ *   IM_EXACT   reference arithmetic order, bit-identical results (the
+ *              default of every wrapper: capi.py, the C++ shim, icemorph)
+ *   IM_FP64    FMA fast path, <= 1e-10 relative to the reference on
+ *              well-conditioned weights
  *   IM_FP32    the pair arithmetic in FP32 (packed FFMA2, two controls per
  *              instruction) with FP64 coordinates, per-tile FP64 sums and
  *              FP64 outputs: <= 1e-5 relative (north star's FP32 mode) on
@@ -105,6 +106,30 @@ double im_eval_wall_function(const im_wall_function* wf, double wall_distance);
  * solve_weights, rbf.hpp:74-76 (rbf.cpp:144-193).  alpha_out: 3n doubles. */
 int im_solve_weights(im_context* ctx, const double* points, const double* displacements,
                      size_t n, im_basis basis, double* alpha_out);
+
+/* assemble_surface_matrix, rbf.hpp:35-36 (rbf.cpp:56-69): the dense kernel
+ * matrix phi(|r_i - r_j|) with unit diagonal, row-major n*n doubles in out. */
+int im_assemble_surface_matrix(im_context* ctx, const double* points, size_t n, im_basis basis,
+                               double* out);
+
+/* CholeskyFactor, rbf.hpp:41-60 (rbf.cpp:71-121): a factor that grows one
+ * row at a time, resident on the device (column-major packed, capacity
+ * doubling).  append: column = the new row's entries against the existing
+ * points followed by the diagonal entry, length size()+1; IM_INVALID_ARGUMENT
+ * "column length must be current size + 1", IM_SOLVE_ERROR "matrix not
+ * numerically positive definite at row k (pivot p)" when the pivot is not
+ * above 1e-14 of the largest diagonal seen (the factor is then unchanged, as
+ * in the reference).  solve: A x = rhs, rhs and x of length size(),
+ * IM_INVALID_ARGUMENT "rhs size does not match factorization" otherwise.
+ * Errors are read with im_last_error(ctx) of the creating context. */
+typedef struct im_cholesky im_cholesky;
+int im_cholesky_create(im_context* ctx, im_cholesky** out);
+int im_cholesky_destroy(im_cholesky* factor);
+size_t im_cholesky_size(const im_cholesky* factor);
+double im_cholesky_smallest_pivot(const im_cholesky* factor);
+int im_cholesky_append(im_cholesky* factor, const double* column, size_t length);
+int im_cholesky_solve(const im_cholesky* factor, const double* rhs, size_t rhs_length, double* x,
+                      size_t x_length);
 
 /* eval_interpolant, rbf.hpp:80-81 (rbf.cpp:195-203), batched over n_query
  * queries.  out: 3 n_query doubles. */

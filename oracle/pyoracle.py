@@ -136,6 +136,19 @@ class Oracle:
         self._check(f(_dp(c), _dp(a), len(c), KINDS.get(kind, kind), R, _dp(q), len(q), _dp(out)))
         return out
 
+    def assemble_surface_matrix(self, points, kind="c2", R=1.0) -> np.ndarray:
+        """ref only: assemble_surface_matrix (rbf.cpp:56-69)."""
+        p = _xyz(points)
+        out = np.zeros((len(p), len(p)))
+        f = self.lib.ref_assemble_surface_matrix
+        f.argtypes = [_pd, _sz, C.c_int, _d, _pd]
+        self._check(f(_dp(p), len(p), KINDS.get(kind, kind), R, _dp(out)))
+        return out
+
+    def cholesky(self) -> "RefCholesky":
+        """ref only: the reference's own CholeskyFactor (rbf.cpp:71-121)."""
+        return RefCholesky(self)
+
     # -- greedy ------------------------------------------------------------
     def greedy_level(self, pos, target, tol, cap=5000, kind="c2", R=1.0, level_index=0):
         pos, tgt = _xyz(pos), _xyz(target)
@@ -370,3 +383,42 @@ class Oracle:
                     cap_hit=caph[:k].astype(bool), target_max=tmax.value,
                     surface_max_error=smax.value, surface_mean_error=smean.value,
                     total_seconds=tsec.value, inverted_elements=int(inv.value))
+
+
+class RefCholesky:
+    """The reference CholeskyFactor through oracle/_ref (ref_cholesky_*)."""
+
+    def __init__(self, orc: Oracle):
+        L = orc.lib
+        self.o, self.L = orc, L
+        L.ref_cholesky_create.restype = C.c_void_p
+        L.ref_cholesky_destroy.argtypes = [C.c_void_p]
+        L.ref_cholesky_size.argtypes = [C.c_void_p]
+        L.ref_cholesky_size.restype = _sz
+        L.ref_cholesky_smallest_pivot.argtypes = [C.c_void_p]
+        L.ref_cholesky_smallest_pivot.restype = _d
+        L.ref_cholesky_append.argtypes = [C.c_void_p, _pd, _sz]
+        L.ref_cholesky_solve.argtypes = [C.c_void_p, _pd, _sz, _pd, _sz]
+        self.h = L.ref_cholesky_create()
+
+    def size(self) -> int:
+        return int(self.L.ref_cholesky_size(self.h))
+
+    def smallest_pivot(self) -> float:
+        return float(self.L.ref_cholesky_smallest_pivot(self.h))
+
+    def append(self, column) -> None:
+        c = np.ascontiguousarray(column, dtype=np.float64).ravel()
+        self.o._check(self.L.ref_cholesky_append(self.h, _dp(c), len(c)))
+
+    def solve(self, rhs) -> np.ndarray:
+        r = np.ascontiguousarray(rhs, dtype=np.float64).ravel()
+        x = np.zeros(self.size())
+        self.o._check(self.L.ref_cholesky_solve(self.h, _dp(r), len(r), _dp(x), len(x)))
+        return x
+
+    def __del__(self):
+        try:
+            self.L.ref_cholesky_destroy(self.h)
+        except Exception:
+            pass

@@ -16,6 +16,8 @@
 //   ref_deform               -> deform                   (pipeline.cpp:19-106)
 //   ref_deform_elements      -> deform with volume elements (report.inverted_elements)
 //   ref_signed_measures      -> signed_measures / count_inverted (quality.cpp:135-148)
+//   ref_assemble_surface_matrix -> assemble_surface_matrix (rbf.cpp:56-69)
+//   ref_cholesky_*           -> CholeskyFactor            (rbf.cpp:71-121)
 //
 // The psi = Wendland-C2 taper (BASELINE cfg1 "psi = Wendland C2 of xi") has
 // no reference implementation; for psi_kind == 1 ref_update_volume restates
@@ -465,5 +467,30 @@ extern "C" int ref_read_su2(const char* path, size_t* sizes, double* xyz, int* k
       }
       for (size_t v : k.nodes) mnodes[pnod++] = v;
     }
+  });
+}
+
+// ---- rbf.hpp:35-60: the dense matrix and the incremental factor ------------
+extern "C" int ref_assemble_surface_matrix(const double* pts, size_t n, int kind, double R,
+                                           double* out) {
+  return guarded([&] {
+    BasisFunction b{kind_of(kind), R};
+    const std::vector<double> m = assemble_surface_matrix(to_vecs(pts, n), b);
+    std::copy(m.begin(), m.end(), out);
+  });
+}
+
+extern "C" void* ref_cholesky_create(void) { return new CholeskyFactor(); }
+extern "C" void ref_cholesky_destroy(void* f) { delete static_cast<CholeskyFactor*>(f); }
+extern "C" size_t ref_cholesky_size(void* f) { return static_cast<CholeskyFactor*>(f)->size(); }
+extern "C" double ref_cholesky_smallest_pivot(void* f) {
+  return static_cast<CholeskyFactor*>(f)->smallest_pivot();
+}
+extern "C" int ref_cholesky_append(void* f, const double* col, size_t len) {
+  return guarded([&] { static_cast<CholeskyFactor*>(f)->append(std::span<const double>(col, len)); });
+}
+extern "C" int ref_cholesky_solve(void* f, const double* rhs, size_t nr, double* x, size_t nx) {
+  return guarded([&] {
+    static_cast<CholeskyFactor*>(f)->solve(std::span<const double>(rhs, nr), std::span<double>(x, nx));
   });
 }

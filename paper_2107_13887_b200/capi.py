@@ -112,7 +112,9 @@ EXPORTS = [
     "im_volume_plan_create", "im_volume_plan_destroy", "im_volume_plan_set_controls",
     "im_volume_plan_run", "im_volume_plan_reset_field", "im_volume_plan_download_field",
     "im_volume_plan_distances", "im_volume_plan_set_level", "im_volume_plan_run_steps",
-    "im_volume_plan_count_support", "im_bench_backward_chain",
+    "im_volume_plan_count_support", "im_bench_backward_chain", "im_assemble_surface_matrix",
+    "im_cholesky_create", "im_cholesky_destroy", "im_cholesky_size", "im_cholesky_smallest_pivot",
+    "im_cholesky_append", "im_cholesky_solve",
 ]
 
 
@@ -174,6 +176,15 @@ def _declare(L):
     L.im_volume_plan_count_support.argtypes = [C.c_void_p, C.c_int, Basis,
                                                C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]
     L.im_bench_backward_chain.argtypes = [C.c_void_p, C.c_int, C.c_int, _pd]
+    L.im_assemble_surface_matrix.argtypes = [C.c_void_p, _pd, _sz, Basis, _pd]
+    L.im_cholesky_create.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    L.im_cholesky_destroy.argtypes = [C.c_void_p]
+    L.im_cholesky_size.argtypes = [C.c_void_p]
+    L.im_cholesky_size.restype = _sz
+    L.im_cholesky_smallest_pivot.argtypes = [C.c_void_p]
+    L.im_cholesky_smallest_pivot.restype = _d
+    L.im_cholesky_append.argtypes = [C.c_void_p, _pd, _sz]
+    L.im_cholesky_solve.argtypes = [C.c_void_p, _pd, _sz, _pd, _sz]
 
 
 def _dp(a):
@@ -282,6 +293,17 @@ class Context:
                                                  _dp(q), len(q), precision, _dp(out)))
         return out
 
+    def assemble_surface_matrix(self, points, kind="c2", R=1.0) -> np.ndarray:
+        """assemble_surface_matrix (rbf.hpp:35-36, rbf.cpp:56-69): n x n, row-major."""
+        p = xyz(points)
+        out = np.zeros((len(p), len(p)))
+        self._check(self.lib.im_assemble_surface_matrix(self.h, _dp(p), len(p), basis(kind, R),
+                                                        _dp(out)))
+        return out
+
+    def cholesky(self) -> "CholeskyFactor":
+        return CholeskyFactor(self)
+
     # -- greedy --------------------------------------------------------------
     def greedy_level(self, pos, target, tol, cap=5000, kind="c2", R=1.0, level_index=0,
                      max_levels=1) -> LevelResult:
@@ -352,7 +374,7 @@ class Context:
         return out
 
     def update_volume(self, nodes, dist, ctrl, alpha, D, psi_kind=0, kind="c2", R=1.0,
-                      precision=FP64, out=None):
+                      precision=EXACT, out=None):
         """update_volume (wall_distance.cpp:46-64): (node ids, values).  ``out``
         = (uint64 ids[n], float64 values[n, 3]) reuses caller buffers (e.g.
         page-locked ones, which the library then fills by direct DMA)."""
@@ -464,7 +486,7 @@ class Context:
 
     def deform(self, nodes, dim, patch, disp, pinned=(), tol=0.1, max_levels=5, cap=5000,
                kind="c2", R=1.0, volume_k=5.0, support_distance=-1.0, psi_kind=0,
-               precision=FP64, elements=None, compute_quality=False):
+               precision=EXACT, elements=None, compute_quality=False):
         nodes, disp = xyz(nodes), xyz(disp)
         patch = np.ascontiguousarray(patch, dtype=np.uint64)
         pinned = np.ascontiguousarray(np.asarray(pinned, dtype=np.uint64).reshape(-1))
@@ -506,6 +528,45 @@ ELEMENT_KINDS = ("line", "triangle", "quadrilateral", "tetrahedron", "hexahedron
                  "pyramid")  # mesh.hpp:15-23 order
 
 
+class CholeskyFactor:
+    """icemorph::CholeskyFactor (rbf.hpp:41-60) resident on the device
+    (im_cholesky_*): append(column) grows the factor by one row, solve(rhs)
+    returns A^-1 rhs, both bit-identical to rbf.cpp:71-121."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+        h = C.c_void_p()
+        ctx._check(ctx.lib.im_cholesky_create(ctx.h, C.byref(h)))
+        self.h = h
+
+    def size(self) -> int:
+        return int(self.ctx.lib.im_cholesky_size(self.h))
+
+    def smallest_pivot(self) -> float:
+        return float(self.ctx.lib.im_cholesky_smallest_pivot(self.h))
+
+    def append(self, column) -> None:
+        c = np.ascontiguousarray(column, dtype=np.float64).ravel()
+        self.ctx._check(self.ctx.lib.im_cholesky_append(self.h, _dp(c), len(c)))
+
+    def solve(self, rhs) -> np.ndarray:
+        r = np.ascontiguousarray(rhs, dtype=np.float64).ravel()
+        x = np.zeros(self.size())
+        self.ctx._check(self.ctx.lib.im_cholesky_solve(self.h, _dp(r), len(r), _dp(x), len(x)))
+        return x
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.im_cholesky_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def elements_csr(elements):
     """Element list -> (kinds int32, offsets uint64, conn uint64) CSR.  Accepts
     a list of (kind, nodes) pairs (kind an int or an ELEMENT_KINDS name) or an
@@ -541,7 +602,7 @@ class VolumePlan:
         c, a = xyz(ctrl), xyz(alpha)
         self.ctx._check(self.ctx.lib.im_volume_plan_set_controls(self.h, _dp(c), _dp(a), len(c)))
 
-    def run(self, D, psi_kind=0, kind="c2", R=1.0, precision=FP64):
+    def run(self, D, psi_kind=0, kind="c2", R=1.0, precision=EXACT):
         wf = WallFunctionC(1.0, D, psi_kind)
         na, ms = _sz(), _d()
         self.ctx._check(self.ctx.lib.im_volume_plan_run(self.h, C.byref(wf), basis(kind, R),
@@ -561,12 +622,12 @@ class VolumePlan:
         self.ctx._check(self.ctx.lib.im_volume_plan_distances(self.h, _dp(out)))
         return out
 
-    def set_level(self, level, ctrl, alpha, D, psi_kind=0, kind="c2", R=1.0, precision=FP64):
+    def set_level(self, level, ctrl, alpha, D, psi_kind=0, kind="c2", R=1.0, precision=EXACT):
         c, a = xyz(ctrl), xyz(alpha)
         self.ctx._check(self.ctx.lib.im_volume_plan_set_level(
             self.h, level, _dp(c), _dp(a), len(c), D, psi_kind, basis(kind, R), precision))
 
-    def run_steps(self, steps, kind="c2", R=1.0, precision=FP64, flush_l2=True) -> dict:
+    def run_steps(self, steps, kind="c2", R=1.0, precision=EXACT, flush_l2=True) -> dict:
         st = np.zeros(10)
         self.ctx._check(self.ctx.lib.im_volume_plan_run_steps(
             self.h, basis(kind, R), precision, steps, int(flush_l2), _dp(st)))

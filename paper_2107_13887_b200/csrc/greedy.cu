@@ -265,6 +265,8 @@ GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap
   ins_ring_ = (size_t)cap * 8 * 5 <= smem_max && !std::getenv("IMB_INSERT_RING2") ? 4
               : (size_t)cap * 8 * 3 <= smem_max                                  ? 2
                                                                                   : 0;
+  if (const char* e = std::getenv("IMB_INSERT_RING0"))
+    if (e[0] == '1') ins_ring_ = 0;  // the global-memory variant, for tests at small sizes
   ins_smem_ = ins_ring_ ? (size_t)cap * 8 * (1 + ins_ring_) : 0;
   if (!ins_ring_) rr_.reserve(cap);
   if (const char* e = std::getenv("IMB_INSERT_T")) ins_threads_ = std::atoi(e);

@@ -58,6 +58,7 @@ struct SpecView {
   SpecCtl* ctl;
   SpecHost* host;
   unsigned long long watchdog_ns;
+  unsigned long long* tl;  // per-step timeline (diagnostics)
 };
 struct SpecStats {
   long long hits = 0, misses = 0, late = 0, rollbacks = 0;
@@ -161,6 +162,7 @@ class GreedyEngine {
   DBuf<double> sp_slots_, sp_fa_, sp_xs_, sp_dwords_, sp_bv2_, sp_fbv_;
   DBuf<int> sp_selstep_, sp_words_, sp_fbi_, sp_bi2_;
   DBuf<SpecCtl> sp_ctl_;
+  DBuf<unsigned long long> sp_tl_;
   SpecHost* sp_host_ = nullptr;
   SpecHost* sp_host_dev_ = nullptr;
   cudaStream_t sp_pred_ = nullptr, sp_chain_ = nullptr;

@@ -74,6 +74,13 @@ __device__ __forceinline__ int4 ld_volatile4(const int* p) {
   return w;
 }
 
+// per-step timeline (diagnostics, IMB_SPEC_LOG): tl[e * (cap + 1) + k]
+enum : int { kTlInsB, kTlInsE, kTlSolveB, kTlSolveE, kTlFsweepE, kTlSweepB, kTlSweepE,
+             kTlChainB, kTlChainE, kTlCount };
+__device__ __forceinline__ void tl_mark(const SpecView& v, int e, int k) {
+  v.tl[(size_t)e * (v.cap + 1) + k] = globaltimer();
+}
+
 __device__ __forceinline__ void st_volatile(int* p, int v) {
   asm volatile("st.volatile.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -122,6 +129,7 @@ __global__ void k_spec_init(SpecView v) {
     v.ins_ep[k] = -1, v.chain_ep[k] = -1, v.ins_node[k] = -1, v.ins_fail[k] = 0;
     v.pred_node[k] = -1, v.pred2_node[k] = -1, v.exact_node[k] = -1;
     v.pred_gap[k] = -1.0, v.exact_gap[k] = -1.0;
+    for (int e = 0; e < kTlCount; ++e) v.tl[(size_t)e * (v.cap + 1) + k] = 0;
   }
   if (t == 0) {
     SpecCtl c{};
@@ -174,7 +182,7 @@ template <int NR, int T>
 __global__ void __launch_bounds__(T) k_spec_insert(SpecView v, int k, int ep) {
   extern __shared__ double sh[];
   __shared__ int s_node, s_exact;
-  if (threadIdx.x == 0) atomicAdd(&v.ctl->probe[0], 1), v.host->seen[0] = k;
+  if (threadIdx.x == 0) atomicAdd(&v.ctl->probe[0], 1), v.host->seen[0] = k, tl_mark(v, kTlInsB, k);
   if (!launch_live(v.ctl, ep)) return;
   if (threadIdx.x == 0) {
     int node = -1, exact = 0;
@@ -206,6 +214,7 @@ __global__ void __launch_bounds__(T) k_spec_insert(SpecView v, int k, int ep) {
   if (threadIdx.x == 0) {
     v.ins_node[k] = node;
     v.pivot[k] = pivot;
+    tl_mark(v, kTlInsE, k);
     if (ok) {
       v.cidx[k] = node;
       v.cx[k] = v.px[node], v.cy[k] = v.py[node], v.cz[k] = v.pz[node];
@@ -236,7 +245,7 @@ __global__ void __launch_bounds__(1024) k_fast_solve(SpecView v, int n, int ep) 
   __shared__ double sb[3][32], rc[32];
   __shared__ double T[32][33];  // T[t][r] = L_{b0+r, b0+t}
   __shared__ int s_ok;
-  if (threadIdx.x == 0) atomicAdd(&v.ctl->probe[1], 1), v.host->seen[1] = n;
+  if (threadIdx.x == 0) atomicAdd(&v.ctl->probe[1], 1), v.host->seen[1] = n, tl_mark(v, kTlSolveB, n);
   if (!launch_live(v.ctl, ep)) return;
   if (threadIdx.x == 0) s_ok = ld_volatile(&v.ins_ep[n - 1]) == ep;
   __syncthreads();
@@ -285,7 +294,7 @@ __global__ void __launch_bounds__(1024) k_fast_solve(SpecView v, int n, int ep) 
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     v.fax[i] = xs[i], v.fay[i] = xs[cap + i], v.faz[i] = xs[2 * cap + i];
-  if (threadIdx.x == 0) v.host->seen[1] = -n;  // diagnostics: finished
+  if (threadIdx.x == 0) v.host->seen[1] = -n, tl_mark(v, kTlSolveE, n);  // diagnostics
 }
 
 __device__ __forceinline__ double fast_wendland(int kind, double eta) {
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep
                        ((volatile int*)v.fbi)[b], ((volatile int*)v.fbi)[gridDim.x + b]});
   v.pred2_node[k] = r.v2 >= 0.0 && r.i2 < n ? r.i2 : -1;
   v.pred_gap[k] = r.v1 > 0.0 ? (r.v1 - fmax(r.v2, 0.0)) / r.v1 : -1.0;
-  atomicAdd(&v.ctl->probe[3], 1), v.host->seen[3] = k;
+  atomicAdd(&v.ctl->probe[3], 1), v.host->seen[3] = k, tl_mark(v, kTlFsweepE, k);
   __threadfence();
   v.pred_node[k] = (r.v1 >= 0.0 && r.i1 < n) ? r.i1 : -1;
 }
@@ -430,7 +439,8 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
   __shared__ double wv[kSweepT / 32], wa[kSweepT / 32], wv2[kSweepT / 32];
   __shared__ int wi[kSweepT / 32], wi2[kSweepT / 32];
   __shared__ bool last;
-  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&v.ctl->probe[5], 1), v.host->seen[5] = k;
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    atomicAdd(&v.ctl->probe[5], 1), v.host->seen[5] = k, tl_mark(v, kTlSweepB, k);
   const bool live_blk = launch_live(v.ctl, ep);  // see k_fast_sweep on the ticket
   const int n = v.n;
   const int slot = k % v.S;
@@ -526,7 +536,7 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
     if (w.x != ep || w.y != 0 || w.w != 0) return;
   }
   const double achieved = v.target_max > 0.0 ? exact::div(ov, v.target_max) : 0.0;
-  atomicAdd(&c->probe[6], 1), v.host->seen[6] = k;
+  atomicAdd(&c->probe[6], 1), v.host->seen[6] = k, tl_mark(v, kTlSweepE, k);
   v.rec_err[k - 1] = achieved;
   v.rec_sec[k - 1] = (double)(globaltimer() - c->t0) * 1e-9;
   v.exact_gap[k] = r.v1 > 0.0 ? (r.v1 - fmax(r.v2, 0.0)) / r.v1 : -1.0;
@@ -631,12 +641,13 @@ __global__ void __launch_bounds__(64) k_chain_server(SpecView v) {
     __syncthreads();
     if (!s_go) return;
     const int kk = s_k, ep = s_ep;
-    if (threadIdx.x == 0) atomicAdd(&v.ctl->probe[7], 1), v.host->seen[7] = kk;
+    if (threadIdx.x == 0) atomicAdd(&v.ctl->probe[7], 1), v.host->seen[7] = kk, tl_mark(v, kTlChainB, kk);
     double* out = v.slots + (size_t)(kk % S) * 3 * v.cap;
     gdev::ChainIO io{v.Lt, (size_t)v.cap, v.diag, v.yx, v.yy, v.yz, out, out + v.cap,
                      out + 2 * v.cap, XS_SMEM ? nullptr : v.xs_global + (size_t)j * 4 * v.cap};
     const bool done = gdev::chain_solve<XS_SMEM, true>(io, kk, sh, SpecAbort{v.ctl, kk, ep});
     if (threadIdx.x == 0 && done) {
+      tl_mark(v, kTlChainE, kk);
       __threadfence();
       st_volatile(&v.chain_ep[kk], ep);
       __threadfence();
@@ -684,6 +695,7 @@ SpecView GreedyEngine::spec_view() {
   s.rec_err = rec_err_.p, s.rec_sec = rec_sec_.p;
   s.ctl = sp_ctl_.p;
   s.host = sp_host_dev_;
+  s.tl = sp_tl_.p;
   const char* we = std::getenv("IMB_SPEC_WATCHDOG_S");
   s.watchdog_ns = (unsigned long long)((we ? std::atof(we) : 60.0) * 1e9);
   return s;
@@ -706,6 +718,7 @@ void GreedyEngine::spec_alloc() {
   sp_fbv_.reserve(2 * (size_t)sp_fnblk_);
   sp_fbi_.reserve(2 * (size_t)sp_fnblk_);
   sp_ctl_.reserve(1);
+  sp_tl_.reserve((size_t)kTlCount * m);
   IMB_CHECK(cudaHostAlloc(&sp_host_, sizeof(SpecHost), cudaHostAllocMapped));
   IMB_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sp_host_dev_), sp_host_, 0));
   // chain server smem: x / D in shared memory when it fits, else global
@@ -900,9 +913,24 @@ const GState& GreedyEngine::run_level_spec() {
                    cap_, fs, c.hits, c.misses, c.late, c.rollbacks);
       // k, predictor gap, exact gap, node inserted at k (last epoch), predicted 1st / 2nd,
       // exact choice
-      for (int k = 1; k <= fs; ++k)
-        std::fprintf(f, "%d %.3e %.3e %d %d %d %d\n", k, pg[k], eg[k], words[3 * m + k],
+      std::vector<unsigned long long> tl((size_t)kTlCount * m);
+      IMB_CHECK(cudaMemcpy(tl.data(), sp_tl_.p, tl.size() * 8, cudaMemcpyDeviceToHost));
+      unsigned long long t0 = ~0ull;
+      for (auto t : tl)
+        if (t) t0 = std::min(t0, t);
+      auto us = [&](int e, int k) -> double {
+        const unsigned long long t = tl[(size_t)e * m + k];
+        return t ? (double)(t - t0) * 1e-3 : -1.0;
+      };
+      // per step: k, gaps, nodes, then the timeline in microseconds from the
+      // level's first event: insert begin/end, fast solve begin/end, fast
+      // sweep end, exact sweep begin/end, chain begin/end (last epoch)
+      for (int k = 1; k <= fs; ++k) {
+        std::fprintf(f, "%d %.3e %.3e %d %d %d %d", k, pg[k], eg[k], words[3 * m + k],
                      words[5 * m + k], words[6 * m + k], words[7 * m + k]);
+        for (int e = 0; e < kTlCount; ++e) std::fprintf(f, " %.1f", us(e, k));
+        std::fprintf(f, "\n");
+      }
       std::fclose(f);
     }
   }
