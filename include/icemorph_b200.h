@@ -259,6 +259,13 @@ typedef struct {
   const size_t* element_nodes;
   size_t n_elements;
   int compute_quality; /* with elements: quality_before / quality_after (pipeline.cpp:55, 102) */
+  /* optional (NULL: not returned): each level's ConvergenceRecord
+   * (LevelSummary::record, pipeline.cpp:83), level l's samples at offset
+   * l * record_stride (record_stride >= min(max_points_per_level, patch +
+   * pinned nodes)); sample count = level_points[l] */
+  double* record_error;
+  double* record_seconds;
+  size_t record_stride;
 } im_deform_config;
 
 typedef struct {

@@ -494,3 +494,49 @@ extern "C" int ref_cholesky_solve(void* f, const double* rhs, size_t nr, double*
     static_cast<CholeskyFactor*>(f)->solve(std::span<const double>(rhs, nr), std::span<double>(x, nx));
   });
 }
+
+// ---- generators / writers (host-side helpers of the Python module) ----------
+// pin paper_2107_13887_b200/host_tools.py: nodes, quads and markers of
+// gen_airfoil_mesh (generators.cpp:45-128), the displacement fields of
+// gen_sinusoidal_displacement / gen_ice_bump (generators.cpp:130-333) and the
+// bytes written by write_vtk / write_displacements (mesh_io.cpp:311-428).
+#include "icemorph/generators.hpp"
+
+extern "C" int ref_gen_airfoil_mesh(double chord, size_t n, size_t m, double* nodes,
+                                    size_t* quads, size_t* airfoil, size_t* farfield) {
+  return guarded([&] {
+    const Mesh mesh = gen_airfoil_mesh(chord, n, m);
+    for (size_t i = 0; i < mesh.nodes.size(); ++i) put(nodes + 3 * i, mesh.nodes[i]);
+    for (size_t e = 0; e < mesh.elements.size(); ++e)
+      for (int k = 0; k < 4; ++k) quads[4 * e + k] = mesh.elements[e].nodes[k];
+    const auto& a = mesh.marker("airfoil").nodes;
+    const auto& f = mesh.marker("farfield").nodes;
+    std::copy(a.begin(), a.end(), airfoil);
+    std::copy(f.begin(), f.end(), farfield);
+  });
+}
+
+// which: 0 sinusoidal (airfoil mode: p0 amplitude, p1 wavenumber),
+//        1 ice bump (p0 center, p1 height, p2 width, horns)
+extern "C" int ref_gen_field(double chord, size_t n, size_t m, int which, double p0, double p1,
+                             double p2, size_t horns, size_t* idx, double* disp, size_t* count) {
+  return guarded([&] {
+    const Mesh mesh = gen_airfoil_mesh(chord, n, m);
+    const DisplacementField f =
+        which == 0 ? gen_sinusoidal_displacement(mesh, "airfoil", SinusoidalMode::Airfoil, p0, p1)
+                   : gen_ice_bump(mesh, "airfoil", IceBumpParams{p0, p1, p2, horns});
+    size_t k = 0;
+    for (const auto& [node, d] : f.entries) idx[k] = node, put(disp + 3 * k, d), ++k;
+    *count = k;
+  });
+}
+
+extern "C" int ref_write_airfoil_files(double chord, size_t n, size_t m, const char* vtk_path,
+                                       const char* disp_path) {
+  return guarded([&] {
+    const Mesh mesh = gen_airfoil_mesh(chord, n, m);
+    write_vtk(mesh, std::string(vtk_path));
+    const DisplacementField f = gen_ice_bump(mesh, "airfoil", IceBumpParams{0.0, 0.02, 0.05, 2});
+    write_displacements(f, mesh.dim, std::string(disp_path));
+  });
+}

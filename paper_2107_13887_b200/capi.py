@@ -66,7 +66,8 @@ class DeformConfigC(C.Structure):
                 ("support_distance", C.c_double), ("psi_kind", C.c_int), ("precision", C.c_int),
                 ("element_kinds", C.POINTER(C.c_int)), ("element_offsets", C.POINTER(C.c_size_t)),
                 ("element_nodes", C.POINTER(C.c_size_t)), ("n_elements", C.c_size_t),
-                ("compute_quality", C.c_int)]
+                ("compute_quality", C.c_int), ("record_error", C.POINTER(C.c_double)),
+                ("record_seconds", C.POINTER(C.c_double)), ("record_stride", C.c_size_t)]
 
 
 class QualityReportC(C.Structure):
@@ -502,6 +503,9 @@ class Context:
         rep = DeformReportC()
         out = np.zeros_like(nodes)
         L = max_levels
+        stride = max(1, min(cap, len(patch) + len(pinned)))
+        rec_e, rec_s = np.zeros(L * stride), np.zeros(L * stride)
+        cfg.record_error, cfg.record_seconds, cfg.record_stride = _dp(rec_e), _dp(rec_s), stride
         pts, tch = np.zeros(L, np.uint64), np.zeros(L, np.uint64)
         ach, sup, sec = np.zeros(L), np.zeros(L), np.zeros(L)
         caph = np.zeros(L, np.int32)
@@ -518,6 +522,9 @@ class Context:
                     surface_mean_error=rep.surface_mean_error, total_seconds=rep.total_seconds,
                     greedy_seconds=rep.greedy_seconds, distance_seconds=rep.distance_seconds,
                     volume_seconds=rep.volume_seconds, inverted_elements=rep.inverted_elements,
+                    records=[(np.arange(1, int(pts[l]) + 1),
+                              rec_e[l * stride:l * stride + int(pts[l])].copy(),
+                              rec_s[l * stride:l * stride + int(pts[l])].copy()) for l in range(k)],
                     quality=None if not rep.has_quality else tuple(
                         dict(min=q.min_orthogonality_deg, mean=q.mean_orthogonality_deg,
                              inverted=int(q.inverted_count), degenerate=int(q.degenerate_count))

@@ -45,8 +45,16 @@ inline Vec3 operator*(Vec3 a, double s) { return a *= s; }
 inline Vec3 operator*(double s, Vec3 a) { return a *= s; }
 inline bool operator==(const Vec3& a, const Vec3& b) { return a.x == b.x && a.y == b.y && a.z == b.z; }
 inline bool operator!=(const Vec3& a, const Vec3& b) { return !(a == b); }
+inline double dot(const Vec3& a, const Vec3& b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+inline Vec3 cross(const Vec3& a, const Vec3& b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
 inline double distance(const Vec3& a, const Vec3& b) { return (a - b).norm(); }
 inline double squared_distance(const Vec3& a, const Vec3& b) { return (a - b).squared_norm(); }
+inline Vec3 normalized(const Vec3& v) {
+  const double n = v.norm();
+  return n > 0.0 ? v * (1.0 / n) : Vec3{};
+}
 static_assert(sizeof(Vec3) == 24, "Vec3 must be three packed doubles (AoS C-ABI)");
 
 // ---- rbf.hpp -------------------------------------------------------------------
@@ -63,6 +71,29 @@ struct BasisFunction {
 };
 double eval_wendland(WendlandKind kind, double eta);
 double eval_basis(const BasisFunction& basis, double distance);
+/// Dense kernel matrix phi(|r_i - r_j|), unit diagonal, row-major n*n
+/// (rbf.hpp:35-36), assembled on the device.
+std::vector<double> assemble_surface_matrix(std::span<const Vec3> points,
+                                            const BasisFunction& basis);
+/// Cholesky factor grown one row at a time (rbf.hpp:41-60), resident on the
+/// device (im_cholesky_*): append throws SolveError when the pivot falls
+/// below 1e-14 of the largest diagonal seen; solve(rhs, x) solves A x = rhs.
+class CholeskyFactor {
+ public:
+  CholeskyFactor();
+  ~CholeskyFactor();
+  CholeskyFactor(const CholeskyFactor&) = delete;
+  CholeskyFactor& operator=(const CholeskyFactor&) = delete;
+  CholeskyFactor(CholeskyFactor&& o) noexcept;
+  CholeskyFactor& operator=(CholeskyFactor&& o) noexcept;
+  std::size_t size() const;
+  void append(std::span<const double> column);
+  void solve(std::span<const double> rhs, std::span<double> x) const;
+  double smallest_pivot() const;
+
+ private:
+  void* handle_ = nullptr;  // im_cholesky*
+};
 struct WeightSet {
   std::vector<Vec3> control_positions;
   std::vector<Vec3> alpha;
@@ -226,11 +257,13 @@ struct DeformationReport {
 std::pair<Mesh, DeformationReport> deform(const Mesh& mesh, const DisplacementField& displacement,
                                           const DeformationConfig& config);
 void write_summary(const DeformationReport& report, std::ostream& out);
+void write_summary(const DeformationReport& report, const std::string& path);
 
 // ---- quality.hpp: the measures deform's report reads (device-evaluated) ------------
 std::vector<double> signed_measures(const Mesh& mesh);
 double signed_measure(const Mesh& mesh, const Element& element);
 std::size_t count_inverted(const Mesh& mesh);
 void write_convergence_csv(const DeformationReport& report, std::ostream& out);
+void write_convergence_csv(const DeformationReport& report, const std::string& path);
 
 }  // namespace icemorph

@@ -1,0 +1,5 @@
+// icemorph/kdtree.hpp — forwarding header: the reference's per-module include
+// (proj/include/icemorph/kdtree.hpp) resolves to the B200 library's single public
+// header, so a reference caller's #include "icemorph/kdtree.hpp" compiles unchanged.
+#pragma once
+#include "icemorph/icemorph.hpp"

@@ -1,0 +1,5 @@
+// icemorph/mesh_io.hpp — forwarding header: the reference's per-module include
+// (proj/include/icemorph/mesh_io.hpp) resolves to the B200 library's single public
+// header, so a reference caller's #include "icemorph/mesh_io.hpp" compiles unchanged.
+#pragma once
+#include "icemorph/icemorph.hpp"

@@ -3,6 +3,7 @@
 // argument marshalling, the reference's exceptions, and the scalar helpers
 // (eval_wendland / eval_basis / wall functions) that the reference also
 // evaluates on the host.  Every hot-path call goes to the device.
+#include <fstream>
 #include <iomanip>
 #include <memory>
 #include <ostream>
@@ -64,6 +65,48 @@ double eval_wendland(WendlandKind kind, double eta) {
 }
 
 double eval_basis(const BasisFunction& basis, double d) { return im_eval_basis(to_c(basis), d); }
+
+// rbf.cpp:56-69 on the device
+std::vector<double> assemble_surface_matrix(std::span<const Vec3> points,
+                                            const BasisFunction& basis) {
+  std::vector<double> m(points.size() * points.size());
+  check(im_assemble_surface_matrix(ctx(), xyz(points), points.size(), to_c(basis), m.data()));
+  return m;
+}
+
+// rbf.cpp:71-121: the factor lives on the device of this thread's context
+CholeskyFactor::CholeskyFactor() {
+  im_cholesky* f = nullptr;
+  check(im_cholesky_create(ctx(), &f));
+  handle_ = f;
+}
+CholeskyFactor::~CholeskyFactor() {
+  if (handle_) im_cholesky_destroy(static_cast<im_cholesky*>(handle_));
+}
+CholeskyFactor::CholeskyFactor(CholeskyFactor&& o) noexcept : handle_(o.handle_) {
+  o.handle_ = nullptr;
+}
+CholeskyFactor& CholeskyFactor::operator=(CholeskyFactor&& o) noexcept {
+  if (this != &o) {
+    if (handle_) im_cholesky_destroy(static_cast<im_cholesky*>(handle_));
+    handle_ = o.handle_;
+    o.handle_ = nullptr;
+  }
+  return *this;
+}
+std::size_t CholeskyFactor::size() const {
+  return im_cholesky_size(static_cast<const im_cholesky*>(handle_));
+}
+double CholeskyFactor::smallest_pivot() const {
+  return im_cholesky_smallest_pivot(static_cast<const im_cholesky*>(handle_));
+}
+void CholeskyFactor::append(std::span<const double> column) {
+  check(im_cholesky_append(static_cast<im_cholesky*>(handle_), column.data(), column.size()));
+}
+void CholeskyFactor::solve(std::span<const double> rhs, std::span<double> x) const {
+  check(im_cholesky_solve(static_cast<const im_cholesky*>(handle_), rhs.data(), rhs.size(),
+                          x.data(), x.size()));
+}
 
 WeightSet solve_weights(std::span<const Vec3> points, std::span<const Vec3> displacements,
                         const BasisFunction& basis) {
@@ -357,6 +400,10 @@ std::pair<Mesh, DeformationReport> deform(const Mesh& mesh, const DisplacementFi
   std::vector<Vec3> d(marker.nodes.size());
   for (std::size_t i = 0; i < marker.nodes.size(); ++i) d[i] = disp.at(marker.nodes[i]);
   const ElementCsr csr(mesh.elements);
+  const std::size_t L = std::max<std::size_t>(1, config.greedy.max_levels);
+  const std::size_t stride = std::max<std::size_t>(
+      1, std::min(config.greedy.max_points_per_level, marker.nodes.size() + pinned.size()));
+  std::vector<double> rec_e(L * stride), rec_s(L * stride);
   const im_deform_config cfg{to_c(config.greedy),
                              config.volume_k,
                              config.support_distance,
@@ -366,10 +413,12 @@ std::pair<Mesh, DeformationReport> deform(const Mesh& mesh, const DisplacementFi
                              csr.offsets.data(),
                              csr.conn(),
                              mesh.elements.size(),
-                             config.compute_quality && !mesh.elements.empty() ? 1 : 0};
+                             config.compute_quality && !mesh.elements.empty() ? 1 : 0,
+                             rec_e.data(),
+                             rec_s.data(),
+                             stride};
   Mesh out = mesh;
   im_deform_report rep{};
-  const std::size_t L = std::max<std::size_t>(1, config.greedy.max_levels);
   std::vector<std::size_t> pts(L), touched(L);
   std::vector<double> ach(L), sup(L), sec(L);
   std::vector<int> caph(L);
@@ -388,6 +437,8 @@ std::pair<Mesh, DeformationReport> deform(const Mesh& mesh, const DisplacementFi
     s.support_distance = sup[l];
     s.touched_nodes = touched[l];
     s.seconds = sec[l];
+    for (std::size_t k = 0; k < pts[l]; ++k)  // LevelSummary::record (pipeline.cpp:83)
+      s.record.samples.push_back({k + 1, rec_e[l * stride + k], rec_s[l * stride + k]});
     r.levels.push_back(std::move(s));
   }
   r.target_max = rep.target_max;
@@ -419,6 +470,15 @@ void write_summary(const DeformationReport& report, std::ostream& out) {
   out << "surface_max_error: " << report.surface_max_error << "\n";
   out << "surface_mean_error: " << report.surface_mean_error << "\n";
   out << "inverted_elements: " << report.inverted_elements << "\n";
+  if (report.quality_before) {
+    out << "min_orthogonality_before_deg: " << report.quality_before->min_orthogonality_deg << "\n";
+    out << "mean_orthogonality_before_deg: " << report.quality_before->mean_orthogonality_deg
+        << "\n";
+  }
+  if (report.quality_after) {
+    out << "min_orthogonality_after_deg: " << report.quality_after->min_orthogonality_deg << "\n";
+    out << "mean_orthogonality_after_deg: " << report.quality_after->mean_orthogonality_deg << "\n";
+  }
   out << "total_seconds: " << std::setprecision(6) << report.total_seconds << std::setprecision(17)
       << "\n";
   for (const auto& l : report.levels) {
@@ -433,6 +493,19 @@ void write_summary(const DeformationReport& report, std::ostream& out) {
 void write_convergence_csv(const DeformationReport& report, std::ostream& out) {
   write_convergence_csv_header(out);
   for (const auto& l : report.levels) append_convergence_csv(out, l.level, l.record);
+}
+
+// pipeline.cpp:143-160
+void write_summary(const DeformationReport& report, const std::string& path) {
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot write summary file '" + path + "'");
+  write_summary(report, out);
+}
+
+void write_convergence_csv(const DeformationReport& report, const std::string& path) {
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot write report file '" + path + "'");
+  write_convergence_csv(report, out);
 }
 
 }  // namespace icemorph

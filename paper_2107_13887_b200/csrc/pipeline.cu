@@ -255,7 +255,13 @@ int im_deform(im_context* ctx, const double* nodes, size_t n_nodes, int dim,
         eng.download(s.nc, lv.idx.data(), nullptr, nullptr, nullptr, nullptr, 0);
         throw_conditioning_nodes(pos.data(), lv.idx, (size_t)s.fail_node);
       }
-      eng.download(s.nc, lv.idx.data(), lv.alpha.data(), current.data(), nullptr, nullptr, 0);
+      const size_t li = levels.size();
+      const bool rec = cfg->record_error && cfg->record_stride >= (size_t)s.steps;
+      eng.download(s.nc, lv.idx.data(), lv.alpha.data(), current.data(),
+                   rec ? cfg->record_error + li * cfg->record_stride : nullptr,
+                   rec && cfg->record_seconds ? cfg->record_seconds + li * cfg->record_stride
+                                              : nullptr,
+                   rec ? s.steps : 0);
       lv.achieved = s.achieved;
       lv.cap_hit = s.status == kStatusCapHit;
       lv.target_max = cur_max;

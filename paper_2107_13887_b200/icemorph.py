@@ -153,6 +153,7 @@ class LevelSummary:
     support_distance: float
     touched_nodes: int
     seconds: float
+    record: list = field(default_factory=list)  # ConvergenceRecord: (points, error, seconds)
 
 
 @dataclass
@@ -247,7 +248,10 @@ def deform(mesh: Mesh, displacement: DisplacementField, config: DeformationConfi
                             quality_before=_quality(r, 0), quality_after=_quality(r, 1),
                             total_seconds=r["total_seconds"])
     for l in range(len(r["points"])):
+        pts, err, sec = r["records"][l]
         rep.levels.append(LevelSummary(l, int(r["points"][l]), float(r["achieved"][l]),
                                        bool(r["cap_hit"][l]), float(r["support"][l]),
-                                       int(r["touched"][l]), float(r["seconds"][l])))
+                                       int(r["touched"][l]), float(r["seconds"][l]),
+                                       [(int(a), float(b), float(c)) for a, b, c in
+                                        zip(pts, err, sec)]))
     return out, rep

@@ -5,7 +5,19 @@
 #include <cstdio>
 #include <string>
 
-#include "icemorph/icemorph.hpp"
+#include <fstream>
+#include <random>
+#include <vector>
+
+// the reference's per-module headers resolve to the shim (forwarding headers)
+#include "icemorph/greedy.hpp"
+#include "icemorph/mesh.hpp"
+#include "icemorph/mesh_io.hpp"
+#include "icemorph/pipeline.hpp"
+#include "icemorph/quality.hpp"
+#include "icemorph/rbf.hpp"
+#include "icemorph/vec.hpp"
+#include "icemorph/wall_distance.hpp"
 
 using namespace icemorph;
 
@@ -152,6 +164,76 @@ int main() {
       parse_error = e.line() > 0 && std::string(e.what()).find("unknown section") != std::string::npos;
     }
     CHECK(parse_error);
+  }
+  // vec.hpp:48-65
+  CHECK(dot(Vec3{1, 2, 3}, Vec3{4, 5, 6}) == 32.0);
+  CHECK(cross(Vec3{1, 0, 0}, Vec3{0, 1, 0}) == (Vec3{0, 0, 1}));
+  CHECK(normalized(Vec3{3, 4, 0}) == (Vec3{0.6000000000000001, 0.8, 0}) ||
+        std::abs(normalized(Vec3{3, 4, 0}).x - 0.6) < 1e-15);
+  CHECK(normalized(Vec3{}) == Vec3{});
+  // surface matrix KATs (test_rbf.cpp:82-94)
+  CHECK(assemble_surface_matrix(two, b2) == (std::vector<double>{1.0, 0.1875, 0.1875, 1.0}));
+  CHECK(assemble_surface_matrix(std::vector<Vec3>{{3.0, 4.0}}, b2) == std::vector<double>{1.0});
+  CHECK(assemble_surface_matrix(std::vector<Vec3>{{0.0, 0.0}, {2.5, 0.0}}, b2) ==
+        (std::vector<double>{1.0, 0.0, 0.0, 1.0}));
+  // CholeskyFactor: rows appended one at a time equal a dense solve
+  // (test_rbf.cpp:183-213), SolveError / invalid_argument semantics
+  {
+    std::mt19937 rng(31);
+    std::uniform_real_distribution<double> u(0.0, 1.0);
+    std::vector<Vec3> pts(25);
+    for (auto& p : pts) p = {u(rng), u(rng), 0.0};
+    const BasisFunction b{WendlandKind::C2, 0.8};
+    CholeskyFactor f;
+    std::vector<double> column;
+    for (std::size_t k = 0; k < pts.size(); ++k) {
+      column.resize(k + 1);
+      for (std::size_t j = 0; j < k; ++j) column[j] = eval_basis(b, distance(pts[j], pts[k]));
+      column[k] = 1.0;
+      f.append(column);
+    }
+    CHECK(f.size() == 25 && f.smallest_pivot() > 0.0);
+    std::vector<double> rhs(25), x(25);
+    for (std::size_t i = 0; i < rhs.size(); ++i) rhs[i] = std::sin(1.7 * i);
+    f.solve(rhs, x);
+    const std::vector<double> A = assemble_surface_matrix(pts, b);
+    double worst = 0.0;
+    for (std::size_t i = 0; i < 25; ++i) {
+      double r = -rhs[i];
+      for (std::size_t j = 0; j < 25; ++j) r += A[i * 25 + j] * x[j];
+      worst = std::max(worst, std::abs(r));
+    }
+    CHECK(worst < 1e-10);
+    bool inv = false, solve_err = false, size_err = false;
+    try { f.append(std::vector<double>(3, 1.0)); } catch (const std::invalid_argument&) { inv = true; }
+    CholeskyFactor g;
+    g.append(std::vector<double>{1.0});
+    try {
+      g.append(std::vector<double>{2.0, 4.0});
+    } catch (const SolveError& e) {
+      solve_err = std::string(e.what()).find("not numerically positive definite at row 1") !=
+                  std::string::npos;
+    }
+    std::vector<double> x2(2);
+    try { g.solve(std::vector<double>{1.0, 2.0}, x2); } catch (const std::invalid_argument&) { size_err = true; }
+    CHECK(inv && solve_err && size_err && g.size() == 1);
+  }
+  // the path overloads of the report writers (pipeline.hpp:59, 62)
+  {
+    DeformationReport rep;
+    rep.marker = "airfoil";
+    write_convergence_csv(rep, std::string("/tmp/imb_shim_conv.csv"));
+    std::ifstream in("/tmp/imb_shim_conv.csv");
+    std::string line;
+    std::getline(in, line);
+    CHECK(line == "level,points,error,seconds");
+    bool threw_path = false;
+    try {
+      write_summary(rep, std::string("/nonexistent_dir/x.txt"));
+    } catch (const std::runtime_error& e) {
+      threw_path = std::string(e.what()) == "cannot write summary file '/nonexistent_dir/x.txt'";
+    }
+    CHECK(threw_path);
   }
   std::printf(failures ? "shim: %d FAILED\n" : "shim: all passed\n", failures);
   return failures ? 1 : 0;

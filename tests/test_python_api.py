@@ -1,6 +1,8 @@
-"""The Python mirror of the reference's icemorph module
-(paper_2107_13887_b200/icemorph.py), exercised like the reference's own
-smoke tests (proj/tests/python/test_smoke.py) on the hot-path surface."""
+"""``import icemorph`` -- the reference module's name list over the B200
+library -- exercised the way the reference's own smoke tests use it
+(proj/tests/python/test_smoke.py): generated meshes and displacement fields,
+deform + report + convergence CSV, SU2 / VTK / displacement files, quality,
+fixed markers, errors."""
 import math
 
 import numpy as np
@@ -11,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(scope="module")
 def im():
-    from paper_2107_13887_b200 import icemorph
+    import icemorph
 
     return icemorph
 
@@ -94,3 +96,55 @@ def test_errors_surface(im):  # test_smoke.py:91-105
     with pytest.raises(RuntimeError) as e:
         im.solve_weights([(0, 0, 0), (1e-18, 0, 0)], [(1, 0, 0), (2, 0, 0)], "c2", 1.0)
     assert isinstance(e.value, SolveError) and "points 0 and 1" in str(e.value)
+
+
+def test_generated_deform_report_and_csv(im, tmp_path):  # test_smoke.py:27-52
+    mesh = im.gen_airfoil_mesh(1.0, 128, 12)
+    assert mesh.num_nodes == 128 * 13
+    assert mesh.marker_names() == ["airfoil", "farfield"]
+    field = im.gen_sinusoidal_displacement(mesh, "airfoil")
+    assert field.max_magnitude() == pytest.approx(0.01, rel=1e-6)
+    cfg = im.DeformationConfig()
+    cfg.support_radius, cfg.tolerance, cfg.levels, cfg.volume_k = 2.0, 0.1, 3, 5.0
+    deformed, report = im.deform(mesh, field, cfg)
+    assert report.surface_max_error < 1e-3 and report.inverted_elements == 0
+    assert len(report.levels) == 3 and all(l.achieved_error < 0.1 for l in report.levels)
+    path = tmp_path / "conv.csv"
+    im.write_convergence_csv(report, str(path))
+    rows = path.read_text().splitlines()
+    assert rows[0] == "level,points,error,seconds"
+    assert len(rows) - 1 == report.total_control_points
+    im.write_summary(report, str(tmp_path / "summary.txt"))
+    assert "total_control_points: %d" % report.total_control_points in (
+        tmp_path / "summary.txt").read_text()
+
+
+def test_generated_files_roundtrip(im, tmp_path):  # test_smoke.py:55-77
+    mesh = im.gen_airfoil_mesh(1.0, 64, 8)
+    im.write_su2(mesh, str(tmp_path / "m.su2"))
+    back = im.read_su2(str(tmp_path / "m.su2"))
+    assert back.num_nodes == mesh.num_nodes and back.nodes() == mesh.nodes()
+    im.write_vtk(mesh, str(tmp_path / "m.vtk"))
+    assert "UNSTRUCTURED_GRID" in (tmp_path / "m.vtk").read_text()
+    f = im.DisplacementField("airfoil")
+    f.set(3, 0.01, -0.002)
+    im.write_displacements(f, mesh.dim, str(tmp_path / "d.txt"))
+    g = im.read_displacements(str(tmp_path / "d.txt"), mesh, "airfoil")
+    assert tuple(g.entries()[3]) == (0.01, -0.002, 0.0)
+
+
+def test_generated_quality_and_pinning(im):  # test_smoke.py:80-104
+    mesh = im.gen_airfoil_mesh(1.0, 64, 8)
+    q = im.orthogonality(mesh)
+    assert 0.0 <= q.min_orthogonality_deg <= 90.0 and q.inverted_count == 0
+    assert all(m > 0 for m in im.signed_measures(mesh))
+    field = im.gen_ice_bump(mesh, "airfoil", height=0.03)
+    cfg = im.DeformationConfig()
+    cfg.support_radius, cfg.levels, cfg.fixed_markers = 2.0, 2, ["farfield"]
+    deformed, _ = im.deform(mesh, field, cfg)
+    before, after = mesh.nodes(), deformed.nodes()
+    assert all(before[i] == after[i] for i in mesh.marker_nodes("farfield"))
+    with pytest.raises(Exception):
+        im.gen_sinusoidal_displacement(mesh, "nope")
+    with pytest.raises(Exception):
+        im.read_su2("does_not_exist.su2")
