@@ -37,13 +37,14 @@ namespace {
 
 constexpr int kT = 1024;
 constexpr size_t kSmemMax = 226 * 1024;
+constexpr size_t kDynMax = 200 * 1024;  // dynamic smem next to the panel kernels' ~25 KB static
 
 // columns of L in flight in shared memory (0: L and the row read from global
 // memory; IMB_INSERT_RING0=1 forces it, for tests at small sizes)
 int ring_for(size_t cap) {
   if (const char* e = std::getenv("IMB_INSERT_RING0"))
     if (e[0] == '1') return 0;
-  return cap * 8 * 5 <= kSmemMax ? 4 : cap * 8 * 3 <= kSmemMax ? 2 : 0;
+  return cap * 8 * 5 <= kDynMax ? 4 : cap * 8 * 3 <= kDynMax ? 2 : 0;
 }
 
 template <int NR>
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(kT) k_chol_forward(const double* Lt, const dou
   extern __shared__ double sh[];
   double* rr = NR > 0 ? sh : rr_global;
   for (int j = threadIdx.x; j < n; j += kT) rr[j] = rhs[j];
-  gdev::forward_subst<NR, kT>(Lt, diag, cap, n, rr, sh + cap);
+  gdev::forward_subst_any<NR, kT>(Lt, diag, cap, n, rr, sh + cap);
   for (int j = threadIdx.x; j < n; j += kT) y[j] = rr[j];
 }
 

@@ -259,9 +259,9 @@ GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap
                                    (int)std::max<size_t>(bw_smem_, 48 * 1024)));
   // k_insert: rr + ring[2] (+ dg staging, which also makes room for y)
   // k_insert: rr + a ring of 4 columns when it fits (cap <= 5812), else 2
-  // k_insert: rr + a ring of 4 columns when it fits (cap <= 5785), else 2
-  // (cap <= 9642), else rr in global memory and L read directly
-  const size_t smem_max = 226 * 1024;
+  // k_insert: rr + 4 columns of staging when it fits (cap <= 5120), else 2
+  // (cap <= 8533), else rr in global memory and L read directly
+  const size_t smem_max = 200 * 1024;  // + ~25 KB static of the panel substitution
   ins_ring_ = (size_t)cap * 8 * 5 <= smem_max && !std::getenv("IMB_INSERT_RING2") ? 4
               : (size_t)cap * 8 * 3 <= smem_max                                  ? 2
                                                                                   : 0;

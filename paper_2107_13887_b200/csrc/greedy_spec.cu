@@ -258,8 +258,20 @@ __global__ void __launch_bounds__(1024) k_fast_solve(SpecView v, int n, int ep) 
       const int i = b0 + warp;
       const double* col = v.Lt + colstart(i, cap) - i;  // col[j] = L_ji
       double sx = 0.0, sy = 0.0, sz = 0.0;
-#pragma unroll 4
-      for (int j = b1 + lane; j < n; j += 32) {
+      int j = b1 + lane;
+      // 8 loads in flight per lane (the column walk is latency-bound otherwise)
+      for (; j + 7 * 32 < n; j += 8 * 32) {
+        double l[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) l[u] = col[j + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int jj = j + 32 * u;
+          sx = fma(l[u], xs[jj], sx), sy = fma(l[u], xs[cap + jj], sy);
+          sz = fma(l[u], xs[2 * cap + jj], sz);
+        }
+      }
+      for (; j < n; j += 32) {
         const double l = col[j];
         sx = fma(l, xs[j], sx), sy = fma(l, xs[cap + j], sy), sz = fma(l, xs[2 * cap + j], sz);
       }
