@@ -158,7 +158,7 @@ class GreedyEngine {
   // speculative pipeline
   bool sp_ready_ = false, sp_xs_smem_ = true;
   int spec_S_ = 32, sp_fnblk_ = 1;
-  size_t sp_server_smem_ = 0, sp_fsolve_smem_ = 0;
+  size_t sp_server_smem_ = 0, sp_fsolve_smem_ = 0, sp_pred_smem_ = 0;
   DBuf<double> sp_slots_, sp_fa_, sp_xs_, sp_dwords_, sp_bv2_, sp_fbv_;
   DBuf<int> sp_selstep_, sp_words_, sp_fbi_, sp_bi2_;
   DBuf<SpecCtl> sp_ctl_;

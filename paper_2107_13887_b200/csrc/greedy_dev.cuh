@@ -146,122 +146,14 @@ __device__ void forward_subst(const double* Lt, const double2* diag, size_t cap,
   __syncthreads();
 }
 
-// Panel form of forward_subst for T-thread CTAs (rr in shared memory): the
-// same per-row operation order (each s_j receives s_j -= L_jm * r_m for m
-// ascending, then r_j = s_j / L_jj, rbf.cpp:80-87), scheduled by panels of
-// 32 rows/columns.  Warp w owns the rows of panels q = w (mod T/32).  For
-// panel p: its owner applies panel p-1 to the panel's rows (from a staged
-// 32x32 block of L), solves the 32x32 diagonal block (lane t divides, a
-// shuffle broadcasts, the lanes below subtract), and publishes the 32 final
-// values through a shared counter; every warp then applies the published
-// panel to its own later rows.  The critical path is ~2-3k cycles per 32
-// columns instead of one CTA barrier per column.
-template <int T>
-__device__ void forward_subst_panel(const double* Lt, const double2* diag, size_t cap, int k,
-                                    double* rr) {
-  constexpr int NW = T / 32;
-  // L_{row in panel p+1, col in panel p} (critical path), double-buffered by
-  // p's parity: the writer of iteration p+2 has seen panel p+1 published,
-  // i.e. its reader is done with the buffer
-  __shared__ double A[2][32][33];
-  __shared__ double D[32][33];  // diagonal block of the panel being solved
-  __shared__ volatile int published;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int P = (k + 31) / 32;
-  if (tid == 0) published = 0;
-  __syncthreads();
-  // column start of m: colstart(m, cap) = m*cap - m*(m-1)/2
-  auto cs = [&](int m) -> size_t { return colstart((size_t)m, cap); };
-  // solve the diagonal block of panel q (owner warp, its rows already up to date)
-  auto solve_block = [&](int q) {
-    const int m0 = 32 * q, cnt = min(32, k - m0);
-    // D[t][lane] = L_{m0+lane, m0+t} for lane > t
-    for (int t = 0; t < cnt; ++t)
-      if (lane > t && lane < cnt) D[t][lane] = Lt[cs(m0 + t) + (lane - t)];
-    const int j = m0 + lane;
-    double s = lane < cnt ? rr[j] : 0.0;
-    const double2 dg = lane < cnt ? diag[j] : make_double2(1.0, 1.0);
-    __syncwarp();
-    for (int t = 0; t < cnt; ++t) {
-      if (lane == t) s = exact::div_rcp(s, exact::Recip{dg.x, dg.y});  // r_t = s / L_tt
-      const double r = __shfl_sync(0xffffffffu, s, t);
-      if (lane > t && lane < cnt) s = exact::sub(s, exact::mul(D[t][lane], r));
-    }
-    if (lane < cnt) rr[j] = s;
-    __syncwarp();
-    __threadfence_block();
-    if (lane == 0) published = q + 1;
-  };
-  // apply published panel p to panel q's rows (q > p), from global L
-  auto apply = [&](int p, int q) {
-    const int m0 = 32 * p, cnt = min(32, k - m0);
-    const int j = 32 * q + lane;
-    if (j >= k) return;
-    double s = rr[j];
-    size_t c = cs(m0);
-    if (cnt == 32) {
-#pragma unroll
-      for (int h = 0; h < 32; h += 16) {
-        double l[16];  // 16 loads in flight, then the ordered chain
-#pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          l[t] = Lt[c + (j - m0 - h - t)];
-          c += cap - (size_t)(m0 + h + t);
-        }
-#pragma unroll
-        for (int t = 0; t < 16; ++t) s = exact::sub(s, exact::mul(l[t], rr[m0 + h + t]));
-      }
-    } else {
-      for (int t = 0; t < cnt; ++t) {
-        s = exact::sub(s, exact::mul(Lt[c + (j - m0 - t)], rr[m0 + t]));
-        c += cap - (size_t)(m0 + t);
-      }
-    }
-    rr[j] = s;
-  };
-  if (warp == 0 && P > 0) solve_block(0);
-  for (int p = 0; p < P; ++p) {
-    const int q1 = p + 1;
-    const bool own_next = q1 < P && q1 % NW == warp;
-    if (own_next) {
-      // stage L_{rows of panel q1, cols of panel p} before the wait (independent of r)
-      const int m0 = 32 * p, cnt = min(32, k - m0), j = 32 * q1 + lane;
-      size_t c = cs(m0);
-      for (int t = 0; t < cnt; ++t) {
-        A[p & 1][t][lane] = j < k ? Lt[c + (j - m0 - t)] : 0.0;
-        c += cap - (size_t)(m0 + t);
-      }
-    }
-    if (lane == 0)
-      while (published <= p) __nanosleep(20);
-    __syncwarp();
-    if (own_next) {
-      const int m0 = 32 * p, cnt = min(32, k - m0), j = 32 * q1 + lane;
-      if (j < k) {
-        double s = rr[j];
-        for (int t = 0; t < cnt; ++t) s = exact::sub(s, exact::mul(A[p & 1][t][lane], rr[m0 + t]));
-        rr[j] = s;
-      }
-      __syncwarp();
-      solve_block(q1);
-    }
-    // my other panels q > p + 1
-    for (int q = warp; q < P; q += NW)
-      if (q > q1) apply(p, q);
-  }
-  __syncthreads();
-}
-
-// forward_subst dispatch: the panel form for large k in wide CTAs (shared
-// rr), the per-column form otherwise (its ring then only needs 64-element
-// slots, k < 64)
+// forward_subst for a single CTA.  (A single SM streams L at only ~30-40
+// GB/s, so the per-column form with its cp.async ring is as fast as a
+// 32-column panel form here; the speculative pipeline's predictor spreads
+// the substitution over a cluster instead, greedy_predict.cuh.)
 template <int NR, int T>
 __device__ void forward_subst_any(const double* Lt, const double2* diag, size_t cap, int k,
                                   double* rr, double* ring) {
-  if (NR > 0 && T >= 256 && k >= 64)
-    forward_subst_panel<T>(Lt, diag, cap, k, rr);
-  else
-    forward_subst<NR, T>(Lt, diag, cap, k, rr, ring, NR > 0 && T >= 256 ? 64 : cap);
+  forward_subst<NR, T>(Lt, diag, cap, k, rr, ring, cap);
 }
 
 struct InsertIO {

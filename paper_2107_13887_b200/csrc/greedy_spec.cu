@@ -46,6 +46,7 @@
 #include "common.cuh"
 #include "greedy.hpp"
 #include "greedy_dev.cuh"
+#include "greedy_predict.cuh"
 
 namespace imb {
 
@@ -307,6 +308,237 @@ __global__ void __launch_bounds__(1024) k_fast_solve(SpecView v, int n, int ep) 
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     v.fax[i] = xs[i], v.fay[i] = xs[cap + i], v.faz[i] = xs[2 * cap + i];
   if (threadIdx.x == 0) v.host->seen[1] = -n, tl_mark(v, kTlSolveE, n);  // diagnostics
+}
+
+
+// ---------------------------------------------------------------------------
+// The predictor step as one cluster kernel: insert(k) + fast_solve(k + 1)
+// (greedy_predict.cuh explains the panel / publish scheme).
+// Dynamic shared memory: rr[cap] | xb[3][cap].
+// ---------------------------------------------------------------------------
+__global__ void __cluster_dims__(pred::kC, 1, 1) __launch_bounds__(pred::kT)
+    k_predict(SpecView v, int k, int ep) {
+  using namespace pred;
+  extern __shared__ __align__(16) double dyn[];
+  __shared__ Smem S;
+  const size_t cap = v.cap;
+  double* rr = dyn;       // [cap]: own rows' running values + every published panel
+  double* xb = dyn + cap;  // [3][cap]: y staging (rank 0), then published x panels
+  const uint32_t rank = ctarank();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    S.fcount = 0, S.bcount = 0, S.ok = 0, S.node = -1, S.exact = 0;
+  }
+  cluster_sync();  // every CTA initialised before any remote write
+  // ---- 0. node: exact if sweep(k) already decided, else the prediction ----
+  if (rank == 0 && tid == 0) {
+    int node = -1, exact = 0;
+    const int4 w = ld_volatile4(&v.ctl->epoch);
+    if (w.x == ep && w.y == 0 && w.w == 0 && (k == 0 || ld_volatile(&v.ins_ep[k - 1]) == ep)) {
+      int cur = ld_volatile(&v.state[k]);
+      if (cur == kEmpty) {
+        const int pn = v.pred_node[k];
+        if (pn >= 0) {
+          const int old = atomicCAS(&v.state[k], kEmpty, pn);
+          cur = old == kEmpty ? pn : old;
+        }
+      }
+      if (cur != kEmpty) exact = (cur & kExactBit) != 0, node = cur & kNodeMask;
+    }
+    atomicAdd(&v.ctl->probe[0], 1), v.host->seen[0] = k, tl_mark(v, kTlInsB, k);
+    if (k == 0) v.ctl->t0 = globaltimer();
+    for (uint32_t c = 0; c < kC; ++c) {
+      st_remote_i(mapa(&S.node, c), node);
+      st_remote_i(mapa(&S.exact, c), exact);
+    }
+  }
+  cluster_sync();
+  const int node = S.node;
+  if (node < 0) return;  // uniform: no prediction / stale launch
+  // ---- 1. the new column for my rows (greedy.cpp:87-93) ----
+  const int P = (k + 31) / 32;
+  auto first_own = [&](int np) { return (int)rank + kC * warp < np ? (int)rank + kC * warp : np; };
+  auto next_own = [&](int q) { return q + kC * kNW; };
+  {
+    const double px = v.px[node], py = v.py[node], pz = v.pz[node];
+    const exact::Recip rR = exact::make_recip(v.R);
+    for (int q = first_own(P); q < P; q = next_own(q)) {
+      const int j = 32 * q + lane;
+      if (j < k) {
+        const double d = exact::dist(v.cx[j], v.cy[j], v.cz[j], px, py, pz);
+        rr[j] = exact::wendland_rt(v.kind, exact::div_rcp(d, rR));
+      }
+    }
+  }
+  __syncwarp();
+  // ---- 2. forward substitution by panels (rbf.cpp:80-87) ----
+  for (int q = first_own(P); q < P; q = next_own(q)) {
+    const int j = 32 * q + lane;
+    double s = j < k ? rr[j] : 0.0;
+    for (int m = 0; m < q; ++m) {
+      const int m0 = 32 * m;  // panels below the last are full
+      double l[32];
+      size_t c = colstart((size_t)m0, cap);
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        l[t] = j < k ? v.Lt[c + (j - m0 - t)] : 0.0;
+        c += cap - (size_t)(m0 + t);
+      }
+      wait_count(&S.fcount, (uint32_t)m + 1);
+#pragma unroll
+      for (int t = 0; t < 32; ++t) s = exact::sub(s, exact::mul(l[t], rr[m0 + t]));
+    }
+    // the 32 x 32 diagonal block, then publish
+    const int m0 = 32 * q, cnt = min(32, k - m0);
+    {
+      size_t c = colstart((size_t)m0, cap);
+      for (int t = 0; t < cnt; ++t) {
+        if (lane > t && lane < cnt) S.D[t][lane] = v.Lt[c + (lane - t)];
+        c += cap - (size_t)(m0 + t);
+      }
+    }
+    const double2 dg = lane < cnt ? v.diag[j] : make_double2(1.0, 1.0);
+    __syncwarp();
+    for (int t = 0; t < cnt; ++t) {
+      if (lane == t) s = exact::div_rcp(s, exact::Recip{dg.x, dg.y});  // r_t = s_t / L_tt
+      const double r = __shfl_sync(0xffffffffu, s, t);
+      if (lane > t && lane < cnt) s = exact::sub(s, exact::mul(S.D[t][lane], r));
+    }
+    if (lane < cnt)
+      for (uint32_t c = 0; c < kC; ++c) st_remote(mapa(&rr[j], c), s);
+    fence_cluster();
+    __syncwarp();
+    if (lane == 0)
+      for (uint32_t c = 0; c < kC; ++c) red_release_add(mapa(&S.fcount, c), 1u);
+  }
+  // ---- 3. y_k, the pivot (rbf.cpp:86-99, 107-112), rank 0 ----
+  if (rank == 0) {
+    wait_count(&S.fcount, (uint32_t)P);
+    __syncthreads();
+    for (int j = tid; j < k; j += kT)
+      xb[j] = v.yx[j], xb[cap + j] = v.yy[j], xb[2 * cap + j] = v.yz[j];
+    __syncthreads();
+    if (tid == 0) {
+      double sq = 0.0, yx = v.tx[node], yy = v.ty[node], yz = v.tz[node];
+#pragma unroll 8
+      for (int j = 0; j < k; ++j) {
+        const double r = rr[j];
+        sq = exact::add(sq, exact::mul(r, r));
+        yx = exact::sub(yx, exact::mul(r, xb[j]));
+        yy = exact::sub(yy, exact::mul(r, xb[cap + j]));
+        yz = exact::sub(yz, exact::mul(r, xb[2 * cap + j]));
+      }
+      const double pivot_sq = exact::sub(1.0, sq);  // column[k] = 1.0, max_diag = 1
+      const double pivot = pivot_sq > 0.0 ? __dsqrt_rn(pivot_sq) : 0.0;
+      const int ok = pivot > exact::mul(1e-14, 1.0);
+      double dk[2] = {pivot, 0.0}, yk[3] = {0.0, 0.0, 0.0};
+      v.ins_node[k] = node;
+      v.pivot[k] = pivot;
+      if (ok) {
+        const exact::Recip pr = exact::make_recip(pivot);
+        dk[1] = pr.y;
+        yk[0] = exact::div_rcp(yx, pr), yk[1] = exact::div_rcp(yy, pr), yk[2] = exact::div_rcp(yz, pr);
+        v.diag[k] = make_double2(pivot, pr.y);
+        v.Lt[colstart((size_t)k, cap)] = pivot;
+        v.yx[k] = yk[0], v.yy[k] = yk[1], v.yz[k] = yk[2];
+      } else {
+        v.ins_fail[k] = 1;
+        if (S.exact) {  // rbf.cpp:92 on the reference's own selection
+          v.ctl->fail_node = node;
+          v.ctl->fail_row = k;
+          v.ctl->fail_pivot = pivot;
+          finish(v, kStatusSolveError, k);
+        }
+      }
+      for (uint32_t c = 0; c < kC; ++c) {
+        st_remote_i(mapa(&S.ok, c), ok);
+        for (int a = 0; a < 3; ++a) st_remote(mapa(&S.yk[a], c), yk[a]);
+        st_remote(mapa(&S.dkk[0], c), dk[0]);
+        st_remote(mapa(&S.dkk[1], c), dk[1]);
+      }
+    }
+  }
+  cluster_sync();
+  if (!S.ok) return;  // uniform
+  // ---- 4. scatter the row into the columns, publish insert(k) ----
+  for (int q = first_own(P); q < P; q = next_own(q)) {
+    const int j = 32 * q + lane;
+    if (j < k) v.Lt[colstart((size_t)j, cap) + (k - j)] = rr[j];
+  }
+  __threadfence();
+  cluster_sync();
+  if (rank == 0 && tid == 0) {
+    v.cidx[k] = node;
+    v.cx[k] = v.px[node], v.cy[k] = v.py[node], v.cz[k] = v.pz[node];
+    v.selstep[node] = k;
+    tl_mark(v, kTlInsE, k);
+    __threadfence();
+    st_volatile(&v.ins_ep[k], ep);  // chain(k + 1) may start
+    if (k + 1 < v.cap) tl_mark(v, kTlSolveB, k + 1);
+  }
+  if (k + 1 >= v.cap) return;  // no prediction is needed past the cap (uniform)
+  // ---- 5. fast backward solve of L^T x = y on n = k + 1 (FMA, any order) ----
+  const int n = k + 1, P2 = (n + 31) / 32;
+  // own panels in decreasing order: the largest own panel first
+  int qtop = first_own(P2);
+  if (qtop < P2)
+    while (next_own(qtop) < P2) qtop = next_own(qtop);
+  for (int q = qtop; q >= 0 && q < P2; q -= kC * kNW) {
+    const int i = 32 * q + lane;
+    const bool live = i < n;
+    double yv[3] = {0.0, 0.0, 0.0};
+    if (live) {
+      if (i == k) yv[0] = S.yk[0], yv[1] = S.yk[1], yv[2] = S.yk[2];
+      else yv[0] = v.yx[i], yv[1] = v.yy[i], yv[2] = v.yz[i];
+    }
+    const size_t ci = live ? colstart((size_t)i, cap) : 0;
+    for (int p = P2 - 1; p > q; --p) {
+      const int j0 = 32 * p, cnt = min(32, n - j0);
+      double l[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) l[t] = live && t < cnt ? v.Lt[ci + (j0 + t - i)] : 0.0;
+      wait_count(&S.bcount, (uint32_t)(P2 - p));
+#pragma unroll
+      for (int t = 0; t < 32; ++t)
+        if (t < cnt) {
+          yv[0] = fma(-l[t], xb[j0 + t], yv[0]);
+          yv[1] = fma(-l[t], xb[cap + j0 + t], yv[1]);
+          yv[2] = fma(-l[t], xb[2 * cap + j0 + t], yv[2]);
+        }
+    }
+    // diagonal block, from the bottom row up
+    const int i0 = 32 * q, cnt = min(32, n - i0);
+    for (int t = 0; t < cnt; ++t)
+      if (lane < t) S.D[t][lane] = v.Lt[colstart((size_t)(i0 + lane), cap) + (t - lane)];
+    const double rc = !live ? 0.0 : (i == k ? S.dkk[1] : v.diag[i].y);
+    __syncwarp();
+    for (int t = cnt - 1; t >= 0; --t) {
+      const double x0 = __shfl_sync(0xffffffffu, yv[0] * rc, t);
+      const double x1 = __shfl_sync(0xffffffffu, yv[1] * rc, t);
+      const double x2 = __shfl_sync(0xffffffffu, yv[2] * rc, t);
+      if (lane == t) yv[0] = x0, yv[1] = x1, yv[2] = x2;
+      if (lane < t) {
+        const double l = S.D[t][lane];
+        yv[0] = fma(-l, x0, yv[0]), yv[1] = fma(-l, x1, yv[1]), yv[2] = fma(-l, x2, yv[2]);
+      }
+    }
+    if (live) {
+      v.fax[i] = yv[0], v.fay[i] = yv[1], v.faz[i] = yv[2];
+      for (uint32_t c = 0; c < kC; ++c) {
+        st_remote(mapa(&xb[i], c), yv[0]);
+        st_remote(mapa(&xb[cap + i], c), yv[1]);
+        st_remote(mapa(&xb[2 * cap + i], c), yv[2]);
+      }
+    }
+    fence_cluster();
+    __syncwarp();
+    if (lane == 0)
+      for (uint32_t c = 0; c < kC; ++c) red_release_add(mapa(&S.bcount, c), 1u);
+  }
+  cluster_sync();  // no CTA leaves while others may still write into it
+  if (rank == 0 && tid == 0) {
+    atomicAdd(&v.ctl->probe[1], 1), v.host->seen[1] = -n, tl_mark(v, kTlSolveE, n);
+  }
 }
 
 __device__ __forceinline__ double fast_wendland(int kind, double eta) {
@@ -743,6 +975,10 @@ void GreedyEngine::spec_alloc() {
   IMB_CHECK(cudaFuncSetAttribute(k_chain_server<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)std::max<size_t>(sp_server_smem_, 48 * 1024)));
   sp_fsolve_smem_ = 3 * (size_t)cap_ * 8;
+  sp_pred_smem_ = 4 * (size_t)cap_ * 8;
+  if (sp_pred_smem_ + sizeof(pred::Smem) + 1024 <= 227 * 1024)
+    IMB_CHECK(cudaFuncSetAttribute(k_predict, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::max<size_t>(sp_pred_smem_, 48 * 1024)));
   IMB_CHECK(cudaFuncSetAttribute(k_fast_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)std::max<size_t>(sp_fsolve_smem_, 48 * 1024)));
   for (auto kern : {k_spec_insert<4, 1024>, k_spec_insert<2, 1024>, k_spec_insert<0, 1024>})
@@ -758,6 +994,7 @@ void GreedyEngine::spec_alloc() {
         (const void*)k_spec_insert<4, 1024>, (const void*)k_spec_insert<2, 1024>,
         (const void*)k_spec_insert<0, 1024>,
         (const void*)k_fast_solve,        (const void*)k_fast_sweep,
+        (const void*)k_predict,
         (const void*)k_spec_wait_chain,   (const void*)k_spec_sweep<-1>,
         (const void*)k_spec_sweep<C0>,    (const void*)k_spec_sweep<C2>,
         (const void*)k_spec_sweep<C4>,    (const void*)k_spec_sweep<C6>,
@@ -804,6 +1041,18 @@ const GState& GreedyEngine::run_level_spec() {
     else
       k_spec_insert<0, 1024><<<1, 1024, 0, sp>>>(v, k, ep);
   };
+  // the cluster predictor (insert(k) + fast_solve(k + 1) in one launch) when
+  // its shared memory fits, else the single-CTA insert and fast solve
+  const bool cluster_pred = sp_pred_smem_ + sizeof(pred::Smem) + 1024 <= 227 * 1024 &&
+                            !std::getenv("IMB_SPEC_NOCLUSTER");
+  auto launch_predict = [&](int k, int ep) {
+    if (cluster_pred) {
+      k_predict<<<pred::kC, pred::kT, sp_pred_smem_, sp>>>(v, k, ep);
+    } else {
+      launch_insert(k, ep);
+      if (k + 1 < cap_) k_fast_solve<<<1, 1024, sp_fsolve_smem_, sp>>>(v, k + 1, ep);
+    }
+  };
   auto launch_sweep = [&](int k, int ep) {
     k_spec_wait_chain<<<1, 1, 0, sm>>>(v, k, ep);
     switch (sweep_kind_) {
@@ -821,13 +1070,11 @@ const GState& GreedyEngine::run_level_spec() {
     const int conf = h->conf;
     while (next <= cap_ && next <= conf + la && !h->abort && !h->done) {
       if (next >= 1) {
-        if (next < cap_) {  // the prediction of c_next feeds insert(next)
-          k_fast_solve<<<1, 1024, sp_fsolve_smem_, sp>>>(v, next, ep);
-          k_fast_sweep<<<fgrid, kFastT, 0, sp>>>(v, next, ep);
-        }
+        // the prediction of c_next (alpha~ from predict(next - 1)) feeds insert(next)
+        if (next < cap_) k_fast_sweep<<<fgrid, kFastT, 0, sp>>>(v, next, ep);
         launch_sweep(next, ep);
       }
-      if (next < cap_) launch_insert(next, ep);
+      if (next < cap_) launch_predict(next, ep);
       IMB_LAUNCH_CHECK();
       ++next;
     }
@@ -842,7 +1089,7 @@ const GState& GreedyEngine::run_level_spec() {
       // restart at the mispredicted step r: sweep(r) is done (c_r is EXACT in
       // state[r]), so only insert(r) is re-issued, then steps r+1.. as usual
       const int r = spec_restart_step();
-      launch_insert(r, ep);
+      launch_predict(r, ep);
       IMB_LAUNCH_CHECK();
       next = r + 1;
       continue;
