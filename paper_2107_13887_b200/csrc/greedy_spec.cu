@@ -372,9 +372,21 @@ __global__ void __cluster_dims__(pred::kC, 1, 1) __launch_bounds__(pred::kT)
   }
   __syncwarp();
   // ---- 2. forward substitution by panels (rbf.cpp:80-87) ----
+  // Staging the diagonal block into the CTA's single S.D before the panel's
+  // last wait is safe: the previous user of S.D (panel q - kC, same CTA) was
+  // solved before panel q - 2 was published, which this warp has waited for.
+  auto stage_fwd_D = [&](int q) {
+    const int m0 = 32 * q, cnt = min(32, k - m0);
+    size_t c = colstart((size_t)m0, cap);
+    for (int t = 0; t < cnt; ++t) {
+      if (lane > t && lane < cnt) S.D[t][lane] = v.Lt[c + (lane - t)];
+      c += cap - (size_t)(m0 + t);
+    }
+  };
   for (int q = first_own(P); q < P; q = next_own(q)) {
     const int j = 32 * q + lane;
     double s = j < k ? rr[j] : 0.0;
+    if (q == 0) stage_fwd_D(q);
     for (int m = 0; m < q; ++m) {
       const int m0 = 32 * m;  // panels below the last are full
       double l[32];
@@ -384,19 +396,13 @@ __global__ void __cluster_dims__(pred::kC, 1, 1) __launch_bounds__(pred::kT)
         l[t] = j < k ? v.Lt[c + (j - m0 - t)] : 0.0;
         c += cap - (size_t)(m0 + t);
       }
+      if (m == q - 1) stage_fwd_D(q);
       wait_count(&S.fcount, (uint32_t)m + 1);
 #pragma unroll
       for (int t = 0; t < 32; ++t) s = exact::sub(s, exact::mul(l[t], rr[m0 + t]));
     }
     // the 32 x 32 diagonal block, then publish
     const int m0 = 32 * q, cnt = min(32, k - m0);
-    {
-      size_t c = colstart((size_t)m0, cap);
-      for (int t = 0; t < cnt; ++t) {
-        if (lane > t && lane < cnt) S.D[t][lane] = v.Lt[c + (lane - t)];
-        c += cap - (size_t)(m0 + t);
-      }
-    }
     const double2 dg = lane < cnt ? v.diag[j] : make_double2(1.0, 1.0);
     __syncwarp();
     for (int t = 0; t < cnt; ++t) {
@@ -406,8 +412,7 @@ __global__ void __cluster_dims__(pred::kC, 1, 1) __launch_bounds__(pred::kT)
     }
     if (lane < cnt)
       for (uint32_t c = 0; c < kC; ++c) st_remote(mapa(&rr[j], c), s);
-    fence_cluster();
-    __syncwarp();
+    __syncwarp();  // orders the lanes' remote stores before lane 0's release
     if (lane == 0)
       for (uint32_t c = 0; c < kC; ++c) red_release_add(mapa(&S.fcount, c), 1u);
   }
@@ -492,11 +497,18 @@ __global__ void __cluster_dims__(pred::kC, 1, 1) __launch_bounds__(pred::kT)
       else yv[0] = v.yx[i], yv[1] = v.yy[i], yv[2] = v.yz[i];
     }
     const size_t ci = live ? colstart((size_t)i, cap) : 0;
+    const int i0 = 32 * q, cnt0 = min(32, n - i0);
+    auto stage_bwd_D = [&]() {  // (same single-buffer argument as the forward pass)
+      for (int t = 0; t < cnt0; ++t)
+        if (lane < t) S.D[t][lane] = v.Lt[colstart((size_t)(i0 + lane), cap) + (t - lane)];
+    };
+    if (q == P2 - 1) stage_bwd_D();
     for (int p = P2 - 1; p > q; --p) {
       const int j0 = 32 * p, cnt = min(32, n - j0);
       double l[32];
 #pragma unroll
       for (int t = 0; t < 32; ++t) l[t] = live && t < cnt ? v.Lt[ci + (j0 + t - i)] : 0.0;
+      if (p == q + 1) stage_bwd_D();
       wait_count(&S.bcount, (uint32_t)(P2 - p));
 #pragma unroll
       for (int t = 0; t < 32; ++t)
@@ -507,9 +519,7 @@ __global__ void __cluster_dims__(pred::kC, 1, 1) __launch_bounds__(pred::kT)
         }
     }
     // diagonal block, from the bottom row up
-    const int i0 = 32 * q, cnt = min(32, n - i0);
-    for (int t = 0; t < cnt; ++t)
-      if (lane < t) S.D[t][lane] = v.Lt[colstart((size_t)(i0 + lane), cap) + (t - lane)];
+    const int cnt = cnt0;
     const double rc = !live ? 0.0 : (i == k ? S.dkk[1] : v.diag[i].y);
     __syncwarp();
     for (int t = cnt - 1; t >= 0; --t) {
@@ -530,7 +540,6 @@ __global__ void __cluster_dims__(pred::kC, 1, 1) __launch_bounds__(pred::kT)
         st_remote(mapa(&xb[2 * cap + i], c), yv[2]);
       }
     }
-    fence_cluster();
     __syncwarp();
     if (lane == 0)
       for (uint32_t c = 0; c < kC; ++c) red_release_add(mapa(&S.bcount, c), 1u);
