@@ -491,7 +491,17 @@ __global__ void __cluster_dims__(pred::kC, 1, 1) __launch_bounds__(pred::kT)
   for (int q = qtop; q >= 0 && q < P2; q -= kC * kNW) {
     const int i = 32 * q + lane;
     const bool live = i < n;
-    double yv[3] = {0.0, 0.0, 0.0};
+    // compensated (double-double) accumulation: the prediction's error then
+    // comes from the rounding of the x values alone, not from the sums'
+    // cancellation (which the ill-conditioned global-support systems amplify)
+    double yv[3] = {0.0, 0.0, 0.0}, yl[3] = {0.0, 0.0, 0.0};
+    auto sub_dd = [&](int a, double l, double x) {  // (yv, yl)[a] -= l * x
+      const double ph = l * x, pl = fma(l, x, -ph);
+      const double t = yv[a] - ph, bb = t - yv[a];
+      const double e = (yv[a] - (t - bb)) + (-ph - bb);
+      yv[a] = t;
+      yl[a] += e - pl;
+    };
     if (live) {
       if (i == k) yv[0] = S.yk[0], yv[1] = S.yk[1], yv[2] = S.yk[2];
       else yv[0] = v.yx[i], yv[1] = v.yy[i], yv[2] = v.yz[i];
@@ -513,9 +523,9 @@ __global__ void __cluster_dims__(pred::kC, 1, 1) __launch_bounds__(pred::kT)
 #pragma unroll
       for (int t = 0; t < 32; ++t)
         if (t < cnt) {
-          yv[0] = fma(-l[t], xb[j0 + t], yv[0]);
-          yv[1] = fma(-l[t], xb[cap + j0 + t], yv[1]);
-          yv[2] = fma(-l[t], xb[2 * cap + j0 + t], yv[2]);
+          sub_dd(0, l[t], xb[j0 + t]);
+          sub_dd(1, l[t], xb[cap + j0 + t]);
+          sub_dd(2, l[t], xb[2 * cap + j0 + t]);
         }
     }
     // diagonal block, from the bottom row up
@@ -523,13 +533,13 @@ __global__ void __cluster_dims__(pred::kC, 1, 1) __launch_bounds__(pred::kT)
     const double rc = !live ? 0.0 : (i == k ? S.dkk[1] : v.diag[i].y);
     __syncwarp();
     for (int t = cnt - 1; t >= 0; --t) {
-      const double x0 = __shfl_sync(0xffffffffu, yv[0] * rc, t);
-      const double x1 = __shfl_sync(0xffffffffu, yv[1] * rc, t);
-      const double x2 = __shfl_sync(0xffffffffu, yv[2] * rc, t);
+      const double x0 = __shfl_sync(0xffffffffu, (yv[0] + yl[0]) * rc, t);
+      const double x1 = __shfl_sync(0xffffffffu, (yv[1] + yl[1]) * rc, t);
+      const double x2 = __shfl_sync(0xffffffffu, (yv[2] + yl[2]) * rc, t);
       if (lane == t) yv[0] = x0, yv[1] = x1, yv[2] = x2;
       if (lane < t) {
         const double l = S.D[t][lane];
-        yv[0] = fma(-l, x0, yv[0]), yv[1] = fma(-l, x1, yv[1]), yv[2] = fma(-l, x2, yv[2]);
+        sub_dd(0, l, x0), sub_dd(1, l, x1), sub_dd(2, l, x2);
       }
     }
     if (live) {
