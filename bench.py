@@ -9,9 +9,11 @@ selection time/level".  `value` is the volume-update throughput in dense-
 equivalent pair evaluations per second (N_active x N_c per level, the count
 the reference evaluates at rbf.cpp:198-201), summed over all ranks.
 
-Workload (default): BASELINE configs[1], the 2-D horn-ice airfoil (10k surface
-points, 1M volume points, R = 0.25c, eps = 1e-4, 3 levels, D = 0.5c), seeded
-synthetic geometry (paper_2107_13887_b200/workloads.py; no dataset exists).
+Workload (default): BASELINE configs[3] (cfg4), the largest single-GPU
+config: the 3-D global wing deformation (100k surface points, 40M volume
+points, R = 40 = 10b, eps = 1e-4, 4 levels, D = inf so every node is
+updated), seeded synthetic geometry (paper_2107_13887_b200/workloads.py; no
+dataset exists).  --workload cfg1|cfg2|cfg3|raw measure the others.
 Setup (untimed): wall distances on the device, then the exact greedy
 multilevel selection on the device (reported as greedy seconds per level).
 A step = the volume update of every level (stable compaction of d < D, then
@@ -55,10 +57,12 @@ METRIC = "volume update Gpair-evals/s & % of FP64 peak; greedy selection time/le
 UNIT = "Gpair-evals/s"
 # algorithmic flops per pair: in support / out of support
 FLOPS = {2: (17.0, 7.0), 3: (22.0, 10.0)}
-# FP64 vector peak measured on this pool's B200 with a DFMA microbenchmark
-# (tools/fp64_probe.cu: 34.2 TFLOP/s at 8 CTAs/SM); MEASURED_PEAKS.json has
-# no FP64 entry.  Nominal 148 SM x 64 DFMA x 2 x 1.965 GHz = 37.2 TFLOP/s.
-FP64_PEAK_TFLOPS = 34.2
+# FP64 vector peak: MEASURED_PEAKS.json has no FP64 entry, so the roofline
+# uses the nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s.  (A
+# DFMA-only microbenchmark on this pool reaches 34.2 TFLOP/s and a DFMA+DMUL
+# mix 98.7 % of nominal, tools/fp64_probe.cu / tools/mix_probe.cu.)
+FP64_PEAK_TFLOPS = 37.2
+FP64_PROBE_TFLOPS = 34.2
 # FP32 (FFMA / packed FFMA2) peak measured with tools/f32_probe.cu on the same
 # pool; nominal 148 SM x 128 lanes x 2 x 1.965 GHz = 74.4 TFLOP/s.
 FP32_PEAK_TFLOPS = 74.4
@@ -299,7 +303,10 @@ def run_b200(args):
                 "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved_tf / peak, 4), "traffic": None,
                 "peak_source": "nominal FP32 (148 SM x 128 lanes x 2 x 1.965 GHz)"
-                if prec == capi.FP32 else "measured DFMA microbenchmark (tools/fp64_probe.cu)",
+                if prec == capi.FP32 else
+                "nominal FP64 (148 SM x 64 DFMA/clk x 2 x 1.965 GHz); MEASURED_PEAKS.json has no "
+                "FP64 entry",
+                "fp64_probe_tflops": FP64_PROBE_TFLOPS,
                 "useful_flops_per_launch": useful_launch,
                 "flops_per_pair_in_support": fin,
                 "in_support_fraction": round(in_step / max(pairs_step, 1), 4),
@@ -316,6 +323,11 @@ def run_b200(args):
     if tr:
         roofline["traffic"] = tr["bytes_per_launch"]
         roofline["traffic_source"] = tr["source"]
+        if tr.get("fp64_pipe_pct") is not None:
+            roofline["ncu_fp64_pipe_active_pct"] = tr["fp64_pipe_pct"]
+
+    # --- the HBM-bound passes (wall distance K6, compaction K7) ---------------
+    hbm = hbm_passes(plan, wl, D, peaks())
 
     # --- e2e through the public C-ABI with host buffers ----------------------
     # inputs and outputs in page-locked host memory (the e2e contract): the
@@ -362,6 +374,7 @@ def run_b200(args):
         "fp64_frac_of_peak": roofline["frac"],
         "kernel_ms_avg": round(kern_ms, 4),
         "wall_distance_ms": round(dist_ms, 3),
+        "hbm_passes": hbm,
         "e2e": e2e,
         "gpu_launches": int(st["launches_per_step"] * args.steps),
         "clocks": clk.summary(),
@@ -377,6 +390,10 @@ def run_b200(args):
         out["deform"] = deform_section(ctx, wl, nodes, dim, surface, R, D, capi)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, levels, d_host, budget_s=args.cpu_seconds)
+        if wl["fixed_controls"] is None and greedy.get("greedy_points_per_level"):
+            out["cpu_baseline"]["greedy"] = cpu_greedy_baseline(
+                wl, greedy["greedy_points_per_level"], greedy["greedy_seconds_per_level"],
+                budget_s=args.cpu_seconds)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -424,6 +441,77 @@ def fast_section(args, plan, levels, wl, R, D, pairs_step, fin, in_step, launche
             "note": "FP32 pair arithmetic (FFMA2), FP64 per-tile sums; bar 1e-5 of max field"
             if prec == capi.FP32 else
             "FMA fast path; agreement limited by the reference weights' conditioning"}
+
+
+def hbm_passes(plan, wl, D, pk):
+    """Achieved HBM GB/s of the wall-distance (K6) and compaction (K7) passes on
+    the headline mesh, against the algorithmic bytes of SURVEY §8(d): 32 B per
+    node for the wall distance (24 B xyz read + 8 B d write), 8 B per node read
+    + 4 B per active node written for the compaction.  With D = inf (cfg4) the
+    step has neither pass, so they run with the cutoff / support distance of 1c
+    (cfg3's D) on the same resident mesh."""
+    Dp = D if math.isfinite(D) else 1.0
+    st = plan.bench_passes(Dp, Dp, reps=5)
+    n = len(wl["nodes"])
+    peak = float(pk.get("hbm_gbs", 6557.1))
+    wd_bytes, cp_bytes = 32.0 * n, 8.0 * n + 4.0 * st["active"]
+    wd = wd_bytes / (st["wall_distance_ms"] * 1e-3) / 1e9
+    cp = cp_bytes / (st["compaction_ms"] * 1e-3) / 1e9
+    return {"wall_distance_ms": round(st["wall_distance_ms"], 3),
+            "wall_distance_gbs": round(wd, 1), "wall_distance_frac_hbm": round(wd / peak, 4),
+            "compaction_ms": round(st["compaction_ms"], 3), "compaction_gbs": round(cp, 1),
+            "compaction_frac_hbm": round(cp / peak, 4), "active_nodes": st["active"],
+            "nodes_within_cutoff": st["within_cutoff"], "cutoff": Dp, "hbm_peak_gbs": peak,
+            "algorithmic_bytes": "wall distance 32 B/node; compaction 8 B/node + 4 B/active"}
+
+
+def cpu_greedy_baseline(wl, device_points, device_seconds, budget_s=12.0):
+    """The reference's own greedy on this box (one core, it is single-threaded):
+    a deterministic prefix of greedy_level (greedy.cpp:60-170) on the full
+    surface, plus its CholeskyFactor append + 3 solves per step (rbf.cpp:71-121)
+    at a larger size, fitted to t(n) = a * N_s * n(n+1)/2 + b * n^3 (sweep +
+    factor/solve) and EXTRAPOLATED to the device's point count per
+    level.  Reported beside the device's measured seconds per level."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    flavour = "ref" if pyoracle.available("ref") else "port"
+    orc = pyoracle.Oracle(flavour)
+    pos, disp = wl["nodes"][wl["surface"]], wl["disp"]
+    ns = len(pos)
+    # prefix sized to ~budget_s of sweep work at ~1.3e8 pair-evals/s
+    K = int(max(50, min(600, math.sqrt(2 * budget_s * 1.3e8 / ns))))
+    t0 = time.perf_counter()
+    g = orc.greedy_level(pos, disp, wl["tol"], K, "c2", wl["R"])
+    t_prefix = time.perf_counter() - t0
+    n_pre = len(g.control_indices)
+    # factor/solve cost per step on a random SPD kernel system
+    b = 0.0
+    if flavour == "ref":
+        m = 400
+        rng = np.random.default_rng(1)
+        pts = rng.random((m, 3))
+        A = orc.assemble_surface_matrix(pts, "c2", 0.9)
+        f = orc.cholesky()
+        t0 = time.perf_counter()
+        for k in range(m):
+            f.append(A[k, :k + 1])
+            for _ in range(3):
+                f.solve(np.ones(k + 1))
+        b = (time.perf_counter() - t0) / sum(k * k for k in range(1, m + 1))  # s per k^2
+    sweep_units = ns * n_pre * (n_pre + 1) / 2.0
+    solve_units = sum(k * k for k in range(1, n_pre + 1))
+    a = max(t_prefix - b * solve_units, 1e-12) / sweep_units
+    est = [a * ns * n * (n + 1) / 2.0 + b * sum(k * k for k in range(1, n + 1)) for n in device_points]
+    return {"unit": "s", "cores": 1, "kind": "reference" if flavour == "ref" else "port",
+            "extrapolated": True,
+            "seconds_per_level": [round(x, 1) for x in est],
+            "seconds_total": round(sum(est), 1),
+            "device_seconds_per_level": device_seconds,
+            "speedup_vs_device": round(sum(est) / max(sum(device_seconds), 1e-9), 1),
+            "sample": f"reference greedy_level prefix of {n_pre} points on the full {ns}-point "
+                      f"surface ({t_prefix:.1f} s) + CholeskyFactor append/3 solves per step, fit "
+                      f"t(n) = a N_s n(n+1)/2 + b sum k^2 (a = {a:.3e} s, b = {b:.3e} s)"}
 
 
 def cpu_baseline(wl, levels, dist, budget_s=12.0, nthreads=None):
@@ -493,6 +581,11 @@ def run_reference(args):
     rng = np.random.default_rng(0)
     if wl["fixed_controls"] is not None:
         levels = [wl["fixed_controls"]]
+    elif not math.isfinite(D):
+        # global support (cfg4): every pair is in support, so the cost depends
+        # only on the control count -- the capped levels' 5000 surface points
+        idx = rng.choice(len(pos), min(len(pos), wl["cap"]), replace=False)
+        levels = [(pos[np.sort(idx)], rng.standard_normal((len(idx), 3)))]
     elif args.workload == "cfg2" and args.scale == 1.0 and os.path.exists(sel):
         z = np.load(sel)
         levels = [(pos[z[f"idx{l}"]], rng.standard_normal((len(z[f"idx{l}"]), 3)) * 1e-3)
@@ -503,8 +596,10 @@ def run_reference(args):
     if wl["dim"] == 2:
         for _, a in levels:
             a[:, 2] = 0.0
-    # wall distances with the reference kd-tree (build_distance_index)
-    dist = orc.build_distance_index(nodes, wl["dim"], surface)
+    # wall distances with the reference kd-tree (build_distance_index); with
+    # D = inf psi == 1 everywhere and every node is active, so none are needed
+    dist = (np.zeros(len(nodes)) if not math.isfinite(D)
+            else orc.build_distance_index(nodes, wl["dim"], surface))
     sample = np.arange(len(nodes))
     vals = []
     for it in range(args.warmup + args.steps):
@@ -528,7 +623,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

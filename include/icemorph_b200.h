@@ -323,6 +323,13 @@ int im_volume_plan_run_steps(im_volume_plan* plan, im_basis basis, int precision
 int im_volume_plan_count_support(im_volume_plan* plan, int level, im_basis basis,
                                  unsigned long long* in_support, unsigned long long* total);
 
+/* The HBM-bound passes on the plan's resident mesh (benchmark): the wall
+ * distance with `cutoff` (into scratch) and the compaction of d < D, each
+ * timed over `reps` passes.  stats (4 doubles): wall-distance ms per pass,
+ * compaction ms per pass, active count at D, nodes within the cutoff. */
+int im_volume_plan_bench_passes(im_volume_plan* plan, double cutoff, double D, int reps,
+                                double* stats);
+
 /* ---- diagnostics ---------------------------------------------------------------
  * Time the exact backward-substitution chain (rbf.cpp:114-120, 3 axes) of
  * size n on a synthetic factor: ms per solve, for the latency roofline. */

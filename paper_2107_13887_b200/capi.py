@@ -115,7 +115,7 @@ EXPORTS = [
     "im_volume_plan_distances", "im_volume_plan_set_level", "im_volume_plan_run_steps",
     "im_volume_plan_count_support", "im_bench_backward_chain", "im_assemble_surface_matrix",
     "im_cholesky_create", "im_cholesky_destroy", "im_cholesky_size", "im_cholesky_smallest_pivot",
-    "im_cholesky_append", "im_cholesky_solve",
+    "im_cholesky_append", "im_cholesky_solve", "im_volume_plan_bench_passes",
 ]
 
 
@@ -177,6 +177,7 @@ def _declare(L):
     L.im_volume_plan_count_support.argtypes = [C.c_void_p, C.c_int, Basis,
                                                C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]
     L.im_bench_backward_chain.argtypes = [C.c_void_p, C.c_int, C.c_int, _pd]
+    L.im_volume_plan_bench_passes.argtypes = [C.c_void_p, _d, _d, C.c_int, _pd]
     L.im_assemble_surface_matrix.argtypes = [C.c_void_p, _pd, _sz, Basis, _pd]
     L.im_cholesky_create.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
     L.im_cholesky_destroy.argtypes = [C.c_void_p]
@@ -640,6 +641,13 @@ class VolumePlan:
             self.h, basis(kind, R), precision, steps, int(flush_l2), _dp(st)))
         return dict(step_ms_total=st[0], kernel_ms_total=st[1], kernel_launches=int(st[2]),
                     launches_per_step=int(st[3]), active=[int(v) for v in st[4:8]])
+
+    def bench_passes(self, cutoff, D, reps=5) -> dict:
+        """Wall-distance (K6) and compaction (K7) passes on the resident mesh."""
+        st = np.zeros(4)
+        self.ctx._check(self.ctx.lib.im_volume_plan_bench_passes(self.h, cutoff, D, reps, _dp(st)))
+        return dict(wall_distance_ms=st[0], compaction_ms=st[1], active=int(st[2]),
+                    within_cutoff=int(st[3]))
 
     def count_support(self, level, kind="c2", R=1.0):
         a, b = C.c_ulonglong(), C.c_ulonglong()

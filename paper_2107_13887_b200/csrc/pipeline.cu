@@ -148,6 +148,9 @@ struct im_volume_plan {
   size_t n = 0;
   int dim = 3;
   DPoints nodes, field;
+  DPoints surf;  // the wall (for the HBM-pass benchmark)
+  size_t n_surface = 0;
+  int sdim = 3;
   DBuf<double> dist, tiles, ctrl_stage;
   DBuf<uint32_t> active;
   size_t nc = 0;
@@ -476,8 +479,10 @@ int im_volume_plan_create(im_context* ctx, const double* nodes, size_t n_nodes, 
     p->field.reserve(n_nodes);
     p->dist.reserve(n_nodes);
     p->active.reserve(n_nodes);
-    DPoints ds;
+    DPoints& ds = p->surf;
     upload_points_indexed(c, nodes, surface, n_surface, ds);
+    p->n_surface = n_surface;
+    p->sdim = dim;
     Timer tm(c.stream);
     if (cutoff < 0.0) {  // D = inf workloads: distances unused (psi == 1)
       IMB_CHECK(cudaMemsetAsync(p->dist.p, 0, n_nodes * 8, c.stream));
@@ -774,6 +779,35 @@ int im_volume_plan_run_steps(im_volume_plan* p, im_basis basis, int precision, i
     stats[1] = kern;
     stats[2] = launches;
     stats[3] = per_step;
+  });
+}
+
+// The HBM-bound passes on the plan's resident mesh, for the bench's
+// roofline: the wall distance (K6, wall_distance.cpp:13-31) of every node
+// with the given cutoff (into scratch, the plan's distances are kept), and
+// the stable compaction of d < D (K7, wall_distance.cpp:56-58), each timed
+// with CUDA events over `reps` passes.  stats: [0] wall-distance ms per pass,
+// [1] compaction ms per pass, [2] active count, [3] nodes with d <= cutoff.
+int im_volume_plan_bench_passes(im_volume_plan* p, double cutoff, double D, int reps,
+                                double* stats) {
+  return guarded(p->ctx, [&](Context& c) {
+    DBuf<double> d;
+    d.reserve(std::max<size_t>(p->n, 1));
+    DBuf<uint32_t> act;
+    act.reserve(std::max<size_t>(p->n, 1));
+    reps = std::max(reps, 1);
+    // warm-up (grid scratch, lazy loading)
+    wall_distance(c, p->nodes, p->n, p->surf, p->n_surface, p->sdim, cutoff, d.p);
+    Timer tw(c.stream);
+    for (int r = 0; r < reps; ++r)
+      wall_distance(c, p->nodes, p->n, p->surf, p->n_surface, p->sdim, cutoff, d.p);
+    stats[0] = tw.ms() / reps;
+    size_t na = compact_active(c, p->dist.p, p->n, D, act.p);
+    Timer tc(c.stream);
+    for (int r = 0; r < reps; ++r) na = compact_active(c, p->dist.p, p->n, D, act.p);
+    stats[1] = tc.ms() / reps;
+    stats[2] = (double)na;
+    stats[3] = (double)compact_active(c, d.p, p->n, std::nextafter(cutoff, INFINITY), act.p);
   });
 }
 
