@@ -127,3 +127,20 @@ def test_plan_wing_slice(gpu, oracle, name):
     D = w.D
     cutoff = D if np.isfinite(D) else -1.0
     _plan_vs_reference(gpu, oracle, nodes, surface, pos[idx], alpha, D, w.psi_kind, R, cutoff)
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_wall_distance_wing_slice(gpu, oracle, name):
+    """build_distance_index (wall_distance.cpp:13-31) on the full wing surface
+    (40k / 100k points, a thin curved shell) for a 150k-node slice of the
+    volume mesh, near and far: equal to the reference kd-tree bit for bit."""
+    pos, disp, R, tol, _ = W.wing_surface_case(name)
+    w = getattr(W, name)()
+    vol = w.nodes[: w.meta["n_volume"]]
+    step = max(1, len(vol) // 150000)
+    nodes = np.ascontiguousarray(np.vstack([vol[::step], pos]))
+    surface = np.arange(len(nodes) - len(pos), len(nodes))
+    dim = 3
+    d0 = oracle.build_distance_index(nodes, dim, surface, nthreads=os.cpu_count() or 1)
+    d1 = gpu.build_distance_index(nodes, dim, surface)
+    assert np.array_equal(d0, d1)
