@@ -63,6 +63,7 @@ constexpr int kNodeMask = kExactBit - 1;
 constexpr int kSweepT = 64;      // exact sweep CTA (one point per thread)
 constexpr int kSweepTile = 128;  // controls per smem tile
 constexpr int kFastT = 128;      // predictor sweep CTA
+constexpr int kFastP = 2;        // points per predictor-sweep thread
 constexpr int kFastTile = 256;
 
 
@@ -560,19 +561,6 @@ __global__ void __cluster_dims__(pred::kC, 1, 1) __launch_bounds__(pred::kT)
   }
 }
 
-__device__ __forceinline__ double fast_wendland(int kind, double eta) {
-  const double u = 1.0 - eta, u2 = u * u;
-  switch (kind) {
-    case C0: return u2;
-    case C2: return u2 * u2 * fma(4.0, eta, 1.0);
-    case C4: return u2 * u2 * u2 * fma(fma(35.0 / 3.0, eta, 6.0), eta, 1.0);
-    default: {
-      const double u4 = u2 * u2;
-      return u4 * u4 * fma(fma(fma(32.0, eta, 25.0), eta, 8.0), eta, 1.0);
-    }
-  }
-}
-
 struct Top2 {
   double v1, v2;
   int i1, i2;
@@ -605,13 +593,27 @@ __device__ __forceinline__ Top2 warp_top2(Top2 t) {
 }
 
 // Predicted argmax of |E|^2 over the candidates (selstep >= k) with the
-// approximate alpha; FMA arithmetic, one point per thread.
+// approximate alpha; FMA arithmetic, kFastP points per thread on coordinates
+// pre-scaled by 1/R (q = |p - c|^2 / R^2), eta from the rsqrt-based sqrt
+// with a second-order correction (fast::sqrt_pos), the support cut as a
+// select.
 //
 // Grid-wide ticket kernels (this one and the exact sweep) never leave a block
 // early: the launch-live flags can flip to dead mid-kernel (an abort / done
 // raised on the other stream), so a dead block skips its work but still takes
 // its ticket, and the last block -- which then also sees the launch dead (the
 // flags are monotone within an epoch) -- resets the ticket and returns.
+template <int KIND>
+__device__ __forceinline__ double fast_phi(double eta) {
+  const double u = 1.0 - eta, u2 = u * u;
+  if (KIND == C0) return u2;
+  if (KIND == C2) return u2 * u2 * fma(4.0, eta, 1.0);
+  if (KIND == C4) return u2 * u2 * u2 * fma(fma(35.0 / 3.0, eta, 6.0), eta, 1.0);
+  const double u4 = u2 * u2;
+  return u4 * u4 * fma(fma(fma(32.0, eta, 25.0), eta, 8.0), eta, 1.0);
+}
+
+template <int KIND>
 __global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep) {
   __shared__ __align__(16) double ct[kFastTile][6];
   __shared__ Top2 wt[kFastT / 32];
@@ -619,35 +621,49 @@ __global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep
   if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&v.ctl->probe[2], 1), v.host->seen[2] = k;
   const bool live_blk = launch_live(v.ctl, ep);
   const int n = v.n;
-  const int i = blockIdx.x * kFastT + threadIdx.x;
-  const bool live = i < n;
-  const double px = live ? v.px[i] : 0.0, py = live ? v.py[i] : 0.0, pz = live ? v.pz[i] : 0.0;
-  const double ir2 = 1.0 / (v.R * v.R);
-  double fx = 0.0, fy = 0.0, fz = 0.0;
+  const double ir = 1.0 / v.R;
+  double px[kFastP], py[kFastP], pz[kFastP], fx[kFastP], fy[kFastP], fz[kFastP];
+#pragma unroll
+  for (int s = 0; s < kFastP; ++s) {
+    const int i = (blockIdx.x * kFastP + s) * kFastT + threadIdx.x;
+    const bool live = i < n;
+    px[s] = live ? v.px[i] * ir : 0.0, py[s] = live ? v.py[i] * ir : 0.0;
+    pz[s] = live ? v.pz[i] * ir : 0.0;
+    fx[s] = fy[s] = fz[s] = 0.0;
+  }
   for (int m0 = 0; live_blk && m0 < k; m0 += kFastTile) {
     const int cnt = min(kFastTile, k - m0);
     __syncthreads();
     for (int t = threadIdx.x; t < cnt; t += kFastT) {
-      ct[t][0] = v.cx[m0 + t], ct[t][1] = v.cy[m0 + t], ct[t][2] = v.cz[m0 + t];
+      ct[t][0] = v.cx[m0 + t] * ir, ct[t][1] = v.cy[m0 + t] * ir, ct[t][2] = v.cz[m0 + t] * ir;
       ct[t][3] = v.fax[m0 + t], ct[t][4] = v.fay[m0 + t], ct[t][5] = v.faz[m0 + t];
     }
     __syncthreads();
-#pragma unroll 4
+#pragma unroll 2
     for (int t = 0; t < cnt; ++t) {
-      const double dx = px - ct[t][0], dy = py - ct[t][1], dz = pz - ct[t][2];
-      const double e2 = fma(dx, dx, fma(dy, dy, dz * dz)) * ir2;
-      if (e2 < 1.0) {
-        const double phi = fast_wendland(v.kind, sqrt(e2));
-        fx = fma(ct[t][3], phi, fx), fy = fma(ct[t][4], phi, fy), fz = fma(ct[t][5], phi, fz);
+      const double2 c01 = *reinterpret_cast<const double2*>(&ct[t][0]);
+      const double2 c23 = *reinterpret_cast<const double2*>(&ct[t][2]);
+      const double2 c45 = *reinterpret_cast<const double2*>(&ct[t][4]);
+#pragma unroll
+      for (int s = 0; s < kFastP; ++s) {
+        const double dx = px[s] - c01.x, dy = py[s] - c01.y, dz = pz[s] - c23.x;
+        const double q = fma(dx, dx, fma(dy, dy, dz * dz));
+        const double eta = fast::sqrt_pos(fmax(q, 1e-300));
+        const double phi = q < 1.0 ? fast_phi<KIND>(eta) : 0.0;
+        fx[s] = fma(c23.y, phi, fx[s]), fy[s] = fma(c45.x, phi, fy[s]), fz[s] = fma(c45.y, phi, fz[s]);
       }
     }
   }
   Top2 t{-1.0, -1.0, n, n};
-  if (live && v.selstep[i] >= k) {
-    const double ex = v.tx[i] - fx, ey = v.ty[i] - fy, ez = v.tz[i] - fz;
-    const double q = fma(ex, ex, fma(ey, ey, ez * ez));
-    t.v1 = q >= 0.0 ? q : 0.0;  // NaN -> 0: a candidate always yields a prediction
-    t.i1 = i;
+#pragma unroll
+  for (int s = 0; s < kFastP; ++s) {
+    const int i = (blockIdx.x * kFastP + s) * kFastT + threadIdx.x;
+    if (i < n && v.selstep[i] >= k) {
+      const double ex = v.tx[i] - fx[s], ey = v.ty[i] - fy[s], ez = v.tz[i] - fz[s];
+      const double q = fma(ex, ex, fma(ey, ey, ez * ez));
+      Top2 u{q >= 0.0 ? q : 0.0, -1.0, i, n};  // NaN -> 0: a candidate always predicts
+      t = merge2(t, u);
+    }
   }
   t = warp_top2(t);
   if ((threadIdx.x & 31) == 0) wt[threadIdx.x >> 5] = t;
@@ -977,7 +993,7 @@ void GreedyEngine::spec_alloc() {
   sp_bi2_.reserve(nblk_);
   sp_dwords_.reserve(3 * m);
   sp_bv2_.reserve(nblk_);
-  sp_fnblk_ = (n_ + 127) / 128;
+  sp_fnblk_ = (n_ + kFastT * kFastP - 1) / (kFastT * kFastP);
   sp_fbv_.reserve(2 * (size_t)sp_fnblk_);
   sp_fbi_.reserve(2 * (size_t)sp_fnblk_);
   sp_ctl_.reserve(1);
@@ -1012,7 +1028,9 @@ void GreedyEngine::spec_alloc() {
         (const void*)k_spec_init,         (const void*)k_spec_rollback,
         (const void*)k_spec_insert<4, 1024>, (const void*)k_spec_insert<2, 1024>,
         (const void*)k_spec_insert<0, 1024>,
-        (const void*)k_fast_solve,        (const void*)k_fast_sweep,
+        (const void*)k_fast_solve,        (const void*)k_fast_sweep<C0>,
+        (const void*)k_fast_sweep<C2>,    (const void*)k_fast_sweep<C4>,
+        (const void*)k_fast_sweep<C6>,
         (const void*)k_predict,
         (const void*)k_spec_wait_chain,   (const void*)k_spec_sweep<-1>,
         (const void*)k_spec_sweep<C0>,    (const void*)k_spec_sweep<C2>,
@@ -1072,6 +1090,14 @@ const GState& GreedyEngine::run_level_spec() {
       if (k + 1 < cap_) k_fast_solve<<<1, 1024, sp_fsolve_smem_, sp>>>(v, k + 1, ep);
     }
   };
+  auto launch_fsweep = [&](int k, int ep) {
+    switch (kind_) {
+      case C0: k_fast_sweep<C0><<<fgrid, kFastT, 0, sp>>>(v, k, ep); break;
+      case C2: k_fast_sweep<C2><<<fgrid, kFastT, 0, sp>>>(v, k, ep); break;
+      case C4: k_fast_sweep<C4><<<fgrid, kFastT, 0, sp>>>(v, k, ep); break;
+      default: k_fast_sweep<C6><<<fgrid, kFastT, 0, sp>>>(v, k, ep); break;
+    }
+  };
   auto launch_sweep = [&](int k, int ep) {
     k_spec_wait_chain<<<1, 1, 0, sm>>>(v, k, ep);
     switch (sweep_kind_) {
@@ -1090,7 +1116,7 @@ const GState& GreedyEngine::run_level_spec() {
     while (next <= cap_ && next <= conf + la && !h->abort && !h->done) {
       if (next >= 1) {
         // the prediction of c_next (alpha~ from predict(next - 1)) feeds insert(next)
-        if (next < cap_) k_fast_sweep<<<fgrid, kFastT, 0, sp>>>(v, next, ep);
+        if (next < cap_) launch_fsweep(next, ep);
         launch_sweep(next, ep);
       }
       if (next < cap_) launch_predict(next, ep);
