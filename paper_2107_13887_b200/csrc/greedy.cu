@@ -39,14 +39,14 @@
 #include "common.cuh"
 #include "greedy.hpp"
 #include "greedy_dev.cuh"
+#include "greedy_sweep.cuh"
 
 namespace imb {
 
 namespace {
 
 constexpr int kInsertThreads = 1024;
-constexpr int kSweepThreads = 64;
-constexpr int kSweepTile = 128;
+constexpr int kSweepThreads = gsw::kT;  // greedy_sweep.cuh: 3 warps x 32 points
 
 using gdev::colstart;
 using gdev::globaltimer;
@@ -112,48 +112,19 @@ template <int KIND>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep(GView g) {
   GState& st = *g.st;
   if (st.status != 0) return;
-  __shared__ __align__(16) double ct[kSweepTile][6];
+  __shared__ __align__(16) gsw::Smem S;
   __shared__ double wv[kSweepThreads / 32], wa[kSweepThreads / 32];
   __shared__ int wi[kSweepThreads / 32];
   __shared__ bool last;
   const int n = g.n, nc = st.nc;
-  const int i = blockIdx.x * kSweepThreads + threadIdx.x;
-  const bool live = i < n;
-  const double px = live ? g.px[i] : 0.0, py = live ? g.py[i] : 0.0, pz = live ? g.pz[i] : 0.0;
-  const exact::Recip rR = exact::make_recip(g.R);
-  double fx = 0.0, fy = 0.0, fz = 0.0;
-  for (int m0 = 0; m0 < nc; m0 += kSweepTile) {
-    const int cnt = min(kSweepTile, nc - m0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < cnt; t += kSweepThreads) {
-      ct[t][0] = g.cx[m0 + t], ct[t][1] = g.cy[m0 + t], ct[t][2] = g.cz[m0 + t];
-      ct[t][3] = g.ax[m0 + t], ct[t][4] = g.ay[m0 + t], ct[t][5] = g.az[m0 + t];
-    }
-    __syncthreads();
-    if (KIND >= 0) {
-      // every thread runs the loop (dead lanes on a zero point: harmless);
-      // past cnt the last control is repeated, evaluated but not summed
-      const double pxa[1] = {px}, pya[1] = {py}, pza[1] = {pz};
-      double fxa[1] = {fx}, fya[1] = {fy}, fza[1] = {fz};
-      for (int t = 0; t < cnt; t += 4) {
-        const int js[4] = {t, min(t + 1, cnt - 1), min(t + 2, cnt - 1), min(t + 3, cnt - 1)};
-        exact_eval<3, KIND < 0 ? C2 : KIND, 1, 4>(&ct[0][0], js, min(4, cnt - t), pxa, pya, pza,
-                                                  fxa, fya, fza, rR);
-      }
-      fx = fxa[0], fy = fya[0], fz = fza[0];
-    } else if (live) {
-      for (int t = 0; t < cnt; ++t) {
-        // distance(surface_positions[i], surface_positions[controls[m]])
-        const double d = exact::dist(px, py, pz, ct[t][0], ct[t][1], ct[t][2]);
-        const double phi = exact::wendland_rt(g.kind, exact::div_rcp(d, rR));
-        if (phi != 0.0) {
-          fx = exact::add(fx, exact::mul(ct[t][3], phi));
-          fy = exact::add(fy, exact::mul(ct[t][4], phi));
-          fz = exact::add(fz, exact::mul(ct[t][5], phi));
-        }
-      }
-    }
-  }
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * gsw::kP + lane;
+  const bool in = i < n;
+  const double px = in ? g.px[i] : 0.0, py = in ? g.py[i] : 0.0, pz = in ? g.pz[i] : 0.0;
+  // greedy_sweep.cuh: phi by all three warps, the ordered sums one axis per warp
+  gsw::interpolant<KIND>(S, g.cx, g.cy, g.cz, g.ax, g.ay, g.az, nc, g.R, g.kind, px, py, pz, true);
+  const bool live = in && threadIdx.x < 32;  // warp 0 owns the points from here on
+  const double fx = S.f[0][lane], fy = S.f[1][lane], fz = S.f[2][lane];
   double nv = -1.0, all = 0.0;
   int ni = n;
   if (live) {
@@ -185,15 +156,31 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(GView g) {
     last = ticket == gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  // final block: grid argmax + decision (greedy.cpp:136-152)
+  if (!last) return;
+  // final block: grid argmax + decision (greedy.cpp:136-152); the block
+  // results are merged by all threads, then across the three warps
   __threadfence();
   double mv = -1.0, ov = 0.0;
   int mi = n;
-  for (int b = 0; b < (int)gridDim.x; ++b) {
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += kSweepThreads) {
     better(mv, mi, ((volatile double*)g.bv)[b], ((volatile int*)g.bi)[b]);
     const double a = ((volatile double*)g.ba)[b];
     ov = (ov < a) ? a : ov;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, mv, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, mi, o);
+    better(mv, mi, v2, i2);
+    const double a2 = __shfl_xor_sync(0xffffffffu, ov, o);
+    ov = (ov < a2) ? a2 : ov;
+  }
+  __syncthreads();  // wv / wi / wa are reused
+  if ((threadIdx.x & 31) == 0) wv[w] = mv, wi[w] = mi, wa[w] = ov;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int t = 1; t < kSweepThreads / 32; ++t) {
+    better(mv, mi, wv[t], wi[t]);
+    ov = (ov < wa[t]) ? wa[t] : ov;
   }
   st.ticket = 0;
   const double achieved = st.target_max > 0.0 ? exact::div(ov, st.target_max) : 0.0;
@@ -236,7 +223,7 @@ GreedyEngine::GreedyEngine(Context& ctx, int n, int cap) : ctx_(ctx), n_(n), cap
   diag_.reserve(cap);
   y_.reserve(cap);
   alpha_.reserve(cap);
-  nblk_ = (n + kSweepThreads - 1) / kSweepThreads;
+  nblk_ = (n + gsw::kP - 1) / gsw::kP;
   bv_.reserve(nblk_);
   ba_.reserve(nblk_);
   bi_.reserve(nblk_);

@@ -47,6 +47,7 @@
 #include "greedy.hpp"
 #include "greedy_dev.cuh"
 #include "greedy_predict.cuh"
+#include "greedy_sweep.cuh"
 
 namespace imb {
 
@@ -60,8 +61,7 @@ namespace {
 constexpr int kEmpty = -1;
 constexpr int kExactBit = 1 << 30;
 constexpr int kNodeMask = kExactBit - 1;
-constexpr int kSweepT = 64;      // exact sweep CTA (one point per thread)
-constexpr int kSweepTile = 128;  // controls per smem tile
+constexpr int kSweepT = gsw::kT;  // exact sweep CTA: 3 warps x 32 points (greedy_sweep.cuh)
 constexpr int kFastT = 128;      // predictor sweep CTA
 constexpr int kFastP = 2;        // points per predictor-sweep thread
 constexpr int kFastTile = 256;
@@ -676,17 +676,24 @@ __global__ void __launch_bounds__(kFastT) k_fast_sweep(SpecView v, int k, int ep
     last = atomicAdd(&v.ctl->fticket, 1) == (int)gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
+  // last block: merge the block results with all threads, then across warps
   __threadfence();
+  Top2 r{-1.0, -1.0, n, n};
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += kFastT)
+    r = merge2(r, Top2{((volatile double*)v.fbv)[b], ((volatile double*)v.fbv2)[b],
+                       ((volatile int*)v.fbi)[b], ((volatile int*)v.fbi)[gridDim.x + b]});
+  r = warp_top2(r);
+  __syncthreads();  // wt is reused
+  if ((threadIdx.x & 31) == 0) wt[threadIdx.x >> 5] = r;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int w = 1; w < kFastT / 32; ++w) r = merge2(r, wt[w]);
   v.ctl->fticket = 0;
   {
     const int4 w = ld_volatile4(&v.ctl->epoch);
     if (w.x != ep || w.y != 0 || w.w != 0) return;
   }
-  Top2 r{-1.0, -1.0, n, n};
-  for (int b = 0; b < (int)gridDim.x; ++b)
-    r = merge2(r, Top2{((volatile double*)v.fbv)[b], ((volatile double*)v.fbv2)[b],
-                       ((volatile int*)v.fbi)[b], ((volatile int*)v.fbi)[gridDim.x + b]});
   v.pred2_node[k] = r.v2 >= 0.0 && r.i2 < n ? r.i2 : -1;
   v.pred_gap[k] = r.v1 > 0.0 ? (r.v1 - fmax(r.v2, 0.0)) / r.v1 : -1.0;
   atomicAdd(&v.ctl->probe[3], 1), v.host->seen[3] = k, tl_mark(v, kTlFsweepE, k);
@@ -714,7 +721,7 @@ __global__ void k_spec_wait_chain(SpecView v, int k, int ep) {
 
 template <int KIND>
 __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int ep) {
-  __shared__ __align__(16) double ct[kSweepTile][6];
+  __shared__ __align__(16) gsw::Smem S;
   __shared__ double wv[kSweepT / 32], wa[kSweepT / 32], wv2[kSweepT / 32];
   __shared__ int wi[kSweepT / 32], wi2[kSweepT / 32];
   __shared__ bool last;
@@ -726,40 +733,14 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
   const double* ax = v.slots + (size_t)slot * 3 * v.cap;
   const double* ay = ax + v.cap;
   const double* az = ay + v.cap;
-  const int i = blockIdx.x * kSweepT + threadIdx.x;
-  const bool live = i < n;
-  const double px = live ? v.px[i] : 0.0, py = live ? v.py[i] : 0.0, pz = live ? v.pz[i] : 0.0;
-  const exact::Recip rR = exact::make_recip(v.R);
-  double fx = 0.0, fy = 0.0, fz = 0.0;
-  for (int m0 = 0; live_blk && m0 < k; m0 += kSweepTile) {
-    const int cnt = min(kSweepTile, k - m0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < cnt; t += kSweepT) {
-      ct[t][0] = v.cx[m0 + t], ct[t][1] = v.cy[m0 + t], ct[t][2] = v.cz[m0 + t];
-      ct[t][3] = ax[m0 + t], ct[t][4] = ay[m0 + t], ct[t][5] = az[m0 + t];
-    }
-    __syncthreads();
-    if (KIND >= 0) {
-      const double pxa[1] = {px}, pya[1] = {py}, pza[1] = {pz};
-      double fxa[1] = {fx}, fya[1] = {fy}, fza[1] = {fz};
-      for (int t = 0; t < cnt; t += 4) {
-        const int js[4] = {t, min(t + 1, cnt - 1), min(t + 2, cnt - 1), min(t + 3, cnt - 1)};
-        exact_eval<3, KIND < 0 ? C2 : KIND, 1, 4>(&ct[0][0], js, min(4, cnt - t), pxa, pya, pza,
-                                                  fxa, fya, fza, rR);
-      }
-      fx = fxa[0], fy = fya[0], fz = fza[0];
-    } else if (live) {
-      for (int t = 0; t < cnt; ++t) {
-        const double d = exact::dist(px, py, pz, ct[t][0], ct[t][1], ct[t][2]);
-        const double phi = exact::wendland_rt(v.kind, exact::div_rcp(d, rR));
-        if (phi != 0.0) {
-          fx = exact::add(fx, exact::mul(ct[t][3], phi));
-          fy = exact::add(fy, exact::mul(ct[t][4], phi));
-          fz = exact::add(fz, exact::mul(ct[t][5], phi));
-        }
-      }
-    }
-  }
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * gsw::kP + lane;
+  const bool in = i < n;
+  const double px = in ? v.px[i] : 0.0, py = in ? v.py[i] : 0.0, pz = in ? v.pz[i] : 0.0;
+  // greedy_sweep.cuh: phi by all three warps, the ordered sums one axis per warp
+  gsw::interpolant<KIND>(S, v.cx, v.cy, v.cz, ax, ay, az, k, v.R, v.kind, px, py, pz, live_blk);
+  const bool live = in && threadIdx.x < 32;  // warp 0 owns the points from here on
+  const double fx = S.f[0][lane], fy = S.f[1][lane], fz = S.f[2][lane];
   double nv = -1.0, all = 0.0, nv2 = -1.0;
   int ni = n, ni2 = n;
   if (live && live_blk) {
@@ -797,16 +778,30 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
     last = atomicAdd(&v.ctl->ticket, 1) == (int)gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  // final block: grid argmax + decision (greedy.cpp:136-152)
+  if (!last) return;
+  // final block: grid argmax + decision (greedy.cpp:136-152); the block
+  // results are merged by all threads, then across the three warps
   __threadfence();
   Top2 r{-1.0, -1.0, n, n};
   double ov = 0.0;
-  for (int b = 0; b < (int)gridDim.x; ++b) {
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += kSweepT) {
     r = merge2(r, Top2{((volatile double*)v.bv)[b], ((volatile double*)v.bv2)[b],
                        ((volatile int*)v.bi)[b], ((volatile int*)v.bi2)[b]});
     const double a = ((volatile double*)v.ba)[b];
     ov = (ov < a) ? a : ov;
+  }
+  r = warp_top2(r);
+  for (int o = 16; o; o >>= 1) {
+    const double a2 = __shfl_xor_sync(0xffffffffu, ov, o);
+    ov = (ov < a2) ? a2 : ov;
+  }
+  __syncthreads();  // the w* arrays are reused
+  if ((threadIdx.x & 31) == 0) wv[w] = r.v1, wi[w] = r.i1, wv2[w] = r.v2, wi2[w] = r.i2, wa[w] = ov;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int t = 1; t < kSweepT / 32; ++t) {
+    r = merge2(r, Top2{wv[t], wv2[t], wi[t], wi2[t]});
+    ov = (ov < wa[t]) ? wa[t] : ov;
   }
   SpecCtl* c = v.ctl;
   c->ticket = 0;

@@ -21,12 +21,17 @@ def ref_update(oracle, nodes, d, ctrl, alpha, D, R, psi=0):
     return oracle.update_volume(nodes, d, ctrl, alpha, D, psi, "c2", R)
 
 
-@pytest.fixture(params=["auto", "no_gather"])
+@pytest.fixture(params=["auto", "gather_tile", "gather_n4", "no_gather"])
 def launch_shape(request, monkeypatch):
-    """Both exact kernels: gathered (R < 15 % of the control spread) and
-    group-culled (IMB_NO_GATHER)."""
+    """Every exact kernel: gathered (R < 15 % of the control spread; the
+    barrier-free default, its 4-controls-per-stage shape and the tile-streaming
+    variant) and group-culled (IMB_NO_GATHER)."""
     if request.param == "no_gather":
         monkeypatch.setenv("IMB_NO_GATHER", "1")
+    elif request.param == "gather_tile":
+        monkeypatch.setenv("IMB_GATHER", "tile")
+    elif request.param == "gather_n4":
+        monkeypatch.setenv("IMB_GATHER", "n4")
     return request.param
 
 
@@ -47,6 +52,34 @@ def test_random_clouds(gpu, oracle, dim, R, launch_shape):
     i0, v0 = ref_update(oracle, nodes, d, ctrl, alpha, 0.8, R)
     i1, v1 = gpu.update_volume(nodes, d, ctrl, alpha, 0.8, 0, "c2", R, capi.EXACT)
     assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("m,scale", [(-2, 1.0), (0, 1.0), (3, 1.0), (-64, 2.0 ** -62), (64, 2.0 ** 63),
+                                     (10, 2.0 ** -300), (-3, 1e-9), (60, 2.0 ** -520), (64, 2.0 ** -440)])
+def test_power_of_two_radius(gpu, oracle, dim, m, scale, launch_shape, monkeypatch):
+    """R = 2^m: the exact kernels pre-scale points and tiles by 1/R and drop
+    the division (volume.cu ScaleTile); eta must not change by a bit, also when
+    the scaled coordinates leave the normal range's comfortable middle
+    (clouds of extent `scale`, so in-support pairs exist only when scale ~ R)."""
+    rng = np.random.default_rng(97 + m + dim)
+    n, nc = 20000, 700
+    nodes = rng.random((n, 3)) * scale
+    ctrl = rng.random((nc, 3)) * scale
+    if dim == 2:
+        nodes[:, 2] = 0.0
+        ctrl[:, 2] = 0.0
+    alpha = rng.standard_normal((nc, 3))
+    if dim == 2:
+        alpha[:, 2] = 0.0
+    d = rng.random(n)
+    R = 2.0 ** m
+    i0, v0 = ref_update(oracle, nodes, d, ctrl, alpha, 0.8, R)
+    i1, v1 = gpu.update_volume(nodes, d, ctrl, alpha, 0.8, 0, "c2", R, capi.EXACT)
+    assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
+    monkeypatch.setenv("IMB_NO_PRESCALE", "1")
+    i2, v2 = gpu.update_volume(nodes, d, ctrl, alpha, 0.8, 0, "c2", R, capi.EXACT)
+    assert np.array_equal(i0, i2) and np.array_equal(v0, v2)
 
 
 def test_boundary_pairs(gpu, oracle, launch_shape):

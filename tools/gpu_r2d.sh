@@ -1,0 +1,30 @@
+# restructured greedy sweeps: parity; timings; ncu of the direct gather kernel, wall distance, k_sweep
+export PYTHONUNBUFFERED=1
+mkdir -p gpurun_out devcache
+cp gpurun_in/*.npz devcache/ 2>/dev/null
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_spec.py tests/test_gpu_wing.py tests/test_gpu_cholesky.py tests/test_gpu_pipeline.py -m gpu -x -q > gpurun_out/pytest_sweep.log 2>&1; echo rc=$? >> gpurun_out/pytest_sweep.log
+tail -n 6 gpurun_out/pytest_sweep.log
+# greedy timings (speculative): cfg2 (3 levels), cfg3 level 0, cfg4 levels 0-1, with the timeline of cfg4
+timeout 600 python tools/greedy_levels.py cfg2 3 > gpurun_out/greedy_cfg2.log 2>&1; tail -2 gpurun_out/greedy_cfg2.log
+timeout 600 python tools/greedy_levels.py cfg3 1 > gpurun_out/greedy_cfg3.log 2>&1; tail -2 gpurun_out/greedy_cfg3.log
+IMB_SPEC_LOG=/tmp/spec_cfg4.log timeout 900 python tools/greedy_levels.py cfg4 2 > gpurun_out/greedy_cfg4.log 2>&1; tail -2 gpurun_out/greedy_cfg4.log
+python tools/spec_timeline.py /tmp/spec_cfg4.log > gpurun_out/spec_timeline_cfg4.txt 2>&1; tail -30 gpurun_out/spec_timeline_cfg4.txt
+gzip -c /tmp/spec_cfg4.log > gpurun_out/spec_cfg4.log.gz
+# sequential engine for the k_sweep capture (plain run first)
+IMB_SPEC=0 timeout 600 python tools/greedy_levels.py cfg2 2 > gpurun_out/greedy_cfg2_seq.log 2>&1 && \
+IMB_SPEC=0 ncu --set full --clock-control none -k regex:"k_sweep" --launch-skip 1200 -c 1 -o /tmp/sw -f python tools/greedy_levels.py cfg2 2 > gpurun_out/ncu_sw.log 2>&1
+ncu -i /tmp/sw.ncu-rep --page raw --csv > gpurun_out/ncu_k_sweep_cfg2_raw.csv 2>/dev/null
+ncu -i /tmp/sw.ncu-rep --page details --csv > gpurun_out/ncu_k_sweep_cfg2_details.csv 2>/dev/null
+# wall distance: launch list + full capture
+timeout 600 python tools/hbm_passes.py cfg3 1.0 1.0 1 > gpurun_out/hbm_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_hbm_cfg3.csv python tools/hbm_passes.py cfg3 1.0 1.0 1 > /dev/null 2>&1
+ncu --set full --clock-control none -k regex:"k_wall_distance" -c 1 -o /tmp/wd -f python tools/hbm_passes.py cfg3 1.0 1.0 1 > gpurun_out/ncu_wd.log 2>&1
+ncu -i /tmp/wd.ncu-rep --page raw --csv > gpurun_out/ncu_k_wall_distance_cfg3_raw.csv 2>/dev/null
+ncu -i /tmp/wd.ncu-rep --page details --csv > gpurun_out/ncu_k_wall_distance_cfg3_details.csv 2>/dev/null
+# the direct gather kernel on cfg3
+timeout 600 python bench.py --workload cfg3 --greedy-cache devcache/cfg3_controls.npz --steps 1 --warmup 1 --no-deform --no-cpu-baseline --no-fast > gpurun_out/bench_cfg3_plain.json 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_volume_exact_direct" --launch-skip 2 -c 1 -o /tmp/gd -f python bench.py --workload cfg3 --greedy-cache devcache/cfg3_controls.npz --steps 1 --warmup 1 --no-deform --no-cpu-baseline --no-fast > gpurun_out/ncu_gd.log 2>&1
+ncu -i /tmp/gd.ncu-rep --page raw --csv > gpurun_out/ncu_k_volume_exact_direct_cfg3_raw.csv 2>/dev/null
+ncu -i /tmp/gd.ncu-rep --page details --csv > gpurun_out/ncu_k_volume_exact_direct_cfg3_details.csv 2>/dev/null
+ncu -i /tmp/gd.ncu-rep --page source --csv > gpurun_out/ncu_k_volume_exact_direct_cfg3_source.csv 2>/dev/null
+du -sh gpurun_out; ls -la gpurun_out | head -40
