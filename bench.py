@@ -174,6 +174,24 @@ def sm_max_mhz(index):
         return 1965.0
 
 
+def exact_division_form(R):
+    """How the exact kernels form eta = d / R (volume.cu exact_prescaled / div2_ok):
+    R = 2^m: coordinates pre-scaled, no division; significand a multiple of 4:
+    the two-operation division; otherwise the three-operation sequence."""
+    m, e = math.frexp(R)
+    if m == 0.5 and -63 <= e <= 65:
+        return "prescaled (R = 2^m, 0 instructions)"
+    if math.isfinite(R) and int(m * 2 ** 53) % 4 == 0:
+        return "two-operation (significand of R a multiple of 4)"
+    return "three-operation"
+
+
+def exact_instructions_per_pair(dim, R):
+    base = 30 if dim == 3 else 25  # with the three-operation division
+    form = exact_division_form(R)
+    return base - 3 if form.startswith("prescaled") else base - 1 if form.startswith("two") else base
+
+
 def ncu_traffic(workload, precision):
     """Per-launch DRAM bytes of the volume kernel from profiles/ncu_traffic.json."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
@@ -311,8 +329,12 @@ def run_b200(args):
                 "flops_per_pair_in_support": fin,
                 "in_support_fraction": round(in_step / max(pairs_step, 1), 4),
                 "dense_equivalent_tflops": round(dense_tf, 3),
-                "fp64_instructions_per_pair": (30 if dim == 3 else 25) if prec == capi.EXACT
+                "fp64_instructions_per_pair": exact_instructions_per_pair(dim, R)
+                if prec == capi.EXACT
                 else 0 if prec == capi.FP32 else (16 if dim == 3 else 14)}
+    if prec == capi.EXACT:
+        roofline["exact_division"] = exact_division_form(R)
+        roofline["instruction_cap_frac"] = round(fin / (2.0 * roofline["fp64_instructions_per_pair"]), 4)
     if prec == capi.FP32:
         roofline["fp32_lane_ops_per_pair"] = 13 if dim == 3 else 10
     # DRAM traffic of the dominant kernel: dram__bytes_read.sum +

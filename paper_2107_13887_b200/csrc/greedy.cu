@@ -46,7 +46,7 @@ namespace imb {
 namespace {
 
 constexpr int kInsertThreads = 1024;
-constexpr int kSweepThreads = gsw::kT;  // greedy_sweep.cuh: 3 warps x 32 points
+constexpr int kSweepThreads = gsw::kT;  // greedy_sweep.cuh: 8 warps x 32 points
 
 using gdev::colstart;
 using gdev::globaltimer;
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(GView g) {
   const int i = blockIdx.x * gsw::kP + lane;
   const bool in = i < n;
   const double px = in ? g.px[i] : 0.0, py = in ? g.py[i] : 0.0, pz = in ? g.pz[i] : 0.0;
-  // greedy_sweep.cuh: phi by all three warps, the ordered sums one axis per warp
+  // greedy_sweep.cuh: phi by all warps, the ordered sums one axis per warp (warps 0-2)
   gsw::interpolant<KIND>(S, g.cx, g.cy, g.cz, g.ax, g.ay, g.az, nc, g.R, g.kind, px, py, pz, true);
   const bool live = in && threadIdx.x < 32;  // warp 0 owns the points from here on
   const double fx = S.f[0][lane], fy = S.f[1][lane], fz = S.f[2][lane];
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(GView g) {
   __syncthreads();
   if (!last) return;
   // final block: grid argmax + decision (greedy.cpp:136-152); the block
-  // results are merged by all threads, then across the three warps
+  // results are merged by all threads, then across the warps
   __threadfence();
   double mv = -1.0, ov = 0.0;
   int mi = n;

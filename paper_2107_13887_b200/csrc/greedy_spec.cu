@@ -61,7 +61,7 @@ namespace {
 constexpr int kEmpty = -1;
 constexpr int kExactBit = 1 << 30;
 constexpr int kNodeMask = kExactBit - 1;
-constexpr int kSweepT = gsw::kT;  // exact sweep CTA: 3 warps x 32 points (greedy_sweep.cuh)
+constexpr int kSweepT = gsw::kT;  // exact sweep CTA: 8 warps x 32 points (greedy_sweep.cuh)
 constexpr int kFastT = 128;      // predictor sweep CTA
 constexpr int kFastP = 2;        // points per predictor-sweep thread
 constexpr int kFastTile = 256;
@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
   const int i = blockIdx.x * gsw::kP + lane;
   const bool in = i < n;
   const double px = in ? v.px[i] : 0.0, py = in ? v.py[i] : 0.0, pz = in ? v.pz[i] : 0.0;
-  // greedy_sweep.cuh: phi by all three warps, the ordered sums one axis per warp
+  // greedy_sweep.cuh: phi by all warps, the ordered sums one axis per warp (warps 0-2)
   gsw::interpolant<KIND>(S, v.cx, v.cy, v.cz, ax, ay, az, k, v.R, v.kind, px, py, pz, live_blk);
   const bool live = in && threadIdx.x < 32;  // warp 0 owns the points from here on
   const double fx = S.f[0][lane], fy = S.f[1][lane], fz = S.f[2][lane];
@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(kSweepT) k_spec_sweep(SpecView v, int k, int e
   __syncthreads();
   if (!last) return;
   // final block: grid argmax + decision (greedy.cpp:136-152); the block
-  // results are merged by all threads, then across the three warps
+  // results are merged by all threads, then across the warps
   __threadfence();
   Top2 r{-1.0, -1.0, n, n};
   double ov = 0.0;

@@ -2,23 +2,27 @@
 // (greedy.cpp:126-134 -> rbf.cpp:195-203), shared by k_sweep (greedy.cu) and
 // k_spec_sweep (greedy_spec.cu).
 //
-// One CTA = 3 warps x 32 surface points.  The reference fixes only the ORDER
+// One CTA = 8 warps x 32 surface points.  The reference fixes only the ORDER
 // OF THE SUM f_p = sum_m alpha_m * phi_pm (insertion order m, one rounding
 // per product and per add); the phi_pm themselves are independent.  So the
 // work is split by stage instead of by point:
-//   stage A  (all 3 warps)  phi for a tile of kSwC controls x 32 points: warp
-//            q evaluates controls q, q+3, ... of the tile (lane = point, the
-//            control's record is a broadcast shared-memory read), four
-//            controls per batch through the staged exact pair arithmetic
-//            (xt::, common.cuh), and stores phi[c][lane];
-//   stage B  (warp q = axis q)  f_q[lane] += alpha_q[c] * phi[c][lane] for
-//            c = 0..cnt-1 in order: the three ordered sums of a point run in
-//            three different warps.
+//   stage A  (all 8 warps)  phi for a tile of kC = 72 controls x 32 points
+//            (lane = point, the control's record is a broadcast shared-memory
+//            read), four or six controls per batch through the staged exact
+//            pair arithmetic (xt::, common.cuh), stored as phi[c][lane]; warps
+//            3-7 take 12 controls each (two batches of six), warps 0-2 only 4
+//            each, because they also run
+//   stage B  (warp q = axis q, q < 3)  f_q[lane] += alpha_q[c] * phi[c][lane]
+//            for c = 0..cnt-1 in order: the three ordered sums of a point run
+//            in three different warps (on three different SM sub-partitions).
+//            12 x 24 = 288 FP64 instructions per A-only warp and tile against
+//            4 x 24 + 72 x 2 = 240 (latency-bound adds) per axis warp: the
+//            warps reach the tile barrier together.
 // Stage B of tile i-1 and stage A of tile i share one barrier interval (phi
 // double-buffered, control records triple-buffered), so the latency-bound
 // ordered adds overlap the throughput-bound pair evaluation.  Against one
 // point per thread (round 1: 2 warps per 64 points, 16 % FP64-pipe activity at
-// N_s = 10k) a 10k-point surface now spreads over 313 CTAs / 939 warps.
+// N_s = 10k) a 10k-point surface now spreads over 313 CTAs / 2504 warps.
 #pragma once
 
 #include "common.cuh"
@@ -26,9 +30,12 @@
 namespace imb {
 namespace gsw {
 
-constexpr int kT = 96;  // threads per CTA (3 warps)
-constexpr int kP = 32;  // surface points per CTA
-constexpr int kC = 48;  // controls per tile (16 per warp)
+constexpr int kW = 8;        // warps per CTA
+constexpr int kT = 32 * kW;  // threads per CTA
+constexpr int kP = 32;       // surface points per CTA
+constexpr int kAxisC = 4;    // stage-A controls of an axis warp (warps 0-2) per tile
+constexpr int kPlainC = 12;  // stage-A controls of the other warps per tile
+constexpr int kC = 3 * kAxisC + (kW - 3) * kPlainC;  // controls per tile (72)
 
 struct Smem {
   double ctl[3][kC][6];  // cx cy cz ax ay az
@@ -97,7 +104,7 @@ __device__ __forceinline__ void interpolant(Smem& S, const double* __restrict__ 
   __syncthreads();
   for (int t = 0; t <= ntiles; ++t) {
     if (t + 1 < ntiles) stage_tile(t + 1);
-    if (t >= 1) {  // stage B: tile t-1, axis q, strictly in control order
+    if (t >= 1 && q < 3) {  // stage B: tile t-1, axis q, strictly in control order
       const int cnt = min(kC, nc - (t - 1) * kC);
       const double* al = &S.ctl[(t - 1) % 3][0][3 + q];
       const double* ph = &S.phi[(t - 1) & 1][0][lane];
@@ -118,23 +125,38 @@ __device__ __forceinline__ void interpolant(Smem& S, const double* __restrict__ 
         }
       }
     }
-    if (t < ntiles) {  // stage A: tile t, controls q, q+3, ... four per batch
+    if (t < ntiles) {  // stage A: tile t, this warp's controls, four per batch
       const int cnt = min(kC, nc - t * kC);
       const double* tile = &S.ctl[t % 3][0][0];
       double* ph = &S.phi[t & 1][0][lane];
-#pragma unroll 1
-      for (int b = q; b < cnt; b += 12) {
-        const int js[4] = {b, min(b + 3, cnt - 1), min(b + 6, cnt - 1), min(b + 9, cnt - 1)};
-        double v[4];
-        phi_batch<KIND, 4>(tile, js, px, py, pz, v, rR, rt_kind);
+      if (q < 3) {  // axis warp: one batch of four
+        const int b = kAxisC * q;
+        if (b < cnt) {
+          const int js[4] = {b, min(b + 1, cnt - 1), min(b + 2, cnt - 1), min(b + 3, cnt - 1)};
+          double v[4];
+          phi_batch<KIND, 4>(tile, js, px, py, pz, v, rR, rt_kind);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (b + 3 * u < cnt) ph[kP * (b + 3 * u)] = v[u];
+          for (int u = 0; u < 4; ++u)
+            if (b + u < cnt) ph[kP * (b + u)] = v[u];
+        }
+      } else {  // two batches of six (six independent dependency chains per lane)
+        const int b0 = 3 * kAxisC + kPlainC * (q - 3);
+#pragma unroll 1
+        for (int b = b0; b < min(cnt, b0 + kPlainC); b += 6) {
+          int js[6];
+#pragma unroll
+          for (int u = 0; u < 6; ++u) js[u] = min(b + u, cnt - 1);
+          double v[6];
+          phi_batch<KIND, 6>(tile, js, px, py, pz, v, rR, rt_kind);
+#pragma unroll
+          for (int u = 0; u < 6; ++u)
+            if (b + u < cnt) ph[kP * (b + u)] = v[u];
+        }
       }
     }
     __syncthreads();
   }
-  S.f[q][lane] = f;
+  if (q < 3) S.f[q][lane] = f;
   __syncthreads();
 }
 

@@ -21,7 +21,7 @@ def ref_update(oracle, nodes, d, ctrl, alpha, D, R, psi=0):
     return oracle.update_volume(nodes, d, ctrl, alpha, D, psi, "c2", R)
 
 
-@pytest.fixture(params=["auto", "gather_tile", "gather_n4", "no_gather"])
+@pytest.fixture(params=["auto", "gather_tile", "gather_n4", "gather_t64", "no_gather"])
 def launch_shape(request, monkeypatch):
     """Every exact kernel: gathered (R < 15 % of the control spread; the
     barrier-free default, its 4-controls-per-stage shape and the tile-streaming
@@ -32,6 +32,8 @@ def launch_shape(request, monkeypatch):
         monkeypatch.setenv("IMB_GATHER", "tile")
     elif request.param == "gather_n4":
         monkeypatch.setenv("IMB_GATHER", "n4")
+    elif request.param == "gather_t64":
+        monkeypatch.setenv("IMB_GATHER", "t64")
     return request.param
 
 
@@ -78,6 +80,26 @@ def test_power_of_two_radius(gpu, oracle, dim, m, scale, launch_shape, monkeypat
     i1, v1 = gpu.update_volume(nodes, d, ctrl, alpha, 0.8, 0, "c2", R, capi.EXACT)
     assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
     monkeypatch.setenv("IMB_NO_PRESCALE", "1")
+    i2, v2 = gpu.update_volume(nodes, d, ctrl, alpha, 0.8, 0, "c2", R, capi.EXACT)
+    assert np.array_equal(i0, i2) and np.array_equal(v0, v2)
+
+
+@pytest.mark.parametrize("R", [40.0, 10.0, 2.5, 1.75, 3.0])
+def test_two_operation_division(gpu, oracle, R, monkeypatch):
+    """Global support with a radius whose significand is a multiple of 4: the
+    3-D kernel forms eta = d / R with exact::div2 (two operations, proven
+    correctly rounded for such divisors, tests/test_div2.py); it must equal
+    the reference and the three-operation form bit for bit."""
+    rng = np.random.default_rng(int(R * 4))
+    n, nc = 40000, 900
+    nodes = rng.random((n, 3)) * [1.0, 1.5, 0.3]
+    ctrl = rng.random((nc, 3)) * [1.0, 1.5, 0.3]
+    alpha = rng.standard_normal((nc, 3))
+    d = rng.random(n)
+    i0, v0 = ref_update(oracle, nodes, d, ctrl, alpha, 0.8, R)
+    i1, v1 = gpu.update_volume(nodes, d, ctrl, alpha, 0.8, 0, "c2", R, capi.EXACT)
+    assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
+    monkeypatch.setenv("IMB_NO_DIV2", "1")
     i2, v2 = gpu.update_volume(nodes, d, ctrl, alpha, 0.8, 0, "c2", R, capi.EXACT)
     assert np.array_equal(i0, i2) and np.array_equal(v0, v2)
 
