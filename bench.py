@@ -367,8 +367,11 @@ def run_b200(args):
         for c, a in levels:
             idx, val = ctx.update_volume(nodes_p, d_p, c, a, D, wl["psi_kind"], "c2", R, prec,
                                          out=out_p)
-            h2d += nodes.nbytes + d_host.nbytes + c.nbytes + a.nbytes
-            d2h += idx.size * 4 + val.nbytes
+            # bytes the library actually moved (its selective upload skips node
+            # chunks without active nodes): counted by the library per call
+            up, down = ctx.last_transfer_bytes
+            h2d += up
+            d2h += down
         if it:  # first pass is warm-up
             e2e_times.append(time.perf_counter() - t0)
     e2e_s = statistics.median(e2e_times)

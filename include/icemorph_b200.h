@@ -89,6 +89,10 @@ int im_context_destroy(im_context* ctx);
 const char* im_last_error(const im_context* ctx);
 /* device time of the last hot-path kernel sequence, milliseconds */
 double im_last_device_ms(const im_context* ctx);
+/* host->device / device->host bytes the last im_update_volume moved (its
+ * selective upload skips node chunks without active nodes); measurement aid */
+void im_last_transfer_bytes(const im_context* ctx, unsigned long long* h2d,
+                            unsigned long long* d2h);
 /* library build tag (sm_100a) */
 const char* im_version(void);
 

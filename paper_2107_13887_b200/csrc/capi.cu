@@ -248,6 +248,10 @@ int im_context_destroy(im_context* ctx) {
 
 const char* im_last_error(const im_context* ctx) { return ctx ? ctx->c.message : "null context"; }
 double im_last_device_ms(const im_context* ctx) { return ctx ? ctx->c.last_kernel_ms : 0.0; }
+void im_last_transfer_bytes(const im_context* ctx, unsigned long long* h2d, unsigned long long* d2h) {
+  if (h2d) *h2d = ctx ? ctx->c.last_h2d_bytes : 0;
+  if (d2h) *d2h = ctx ? ctx->c.last_d2h_bytes : 0;
+}
 
 double im_eval_wendland(int kind, double eta) { return h_wendland(kind, eta); }
 double im_eval_basis(im_basis b, double distance) {
@@ -644,6 +648,8 @@ void update_volume_selective(Context& c, const double* nodes, size_t n_nodes, co
       std::memcpy(entry_values + 3 * k0, pin_vals + 3 * k0, 24 * (k1 - k0));
     });
   tr.mark("values down");
+  c.last_h2d_bytes = 8ull * n_nodes + 24ull * uploaded + 48ull * nc;
+  c.last_d2h_bytes = 28ull * na;
   if (std::getenv("IMB_TRACE"))
     std::fprintf(stderr, "[imb]   selective upload: %zu of %zu nodes in %zu-node chunks, %zu active\n",
                  uploaded, n_nodes, chunk, na);
@@ -773,6 +779,7 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     PhaseTrace tr(c.stream);
     check_kind(basis.kind);
     *n_entries = 0;
+    c.last_h2d_bytes = c.last_d2h_bytes = 0;
     const double D = wf->support_distance;
     if (D <= 0.0 || n_nodes == 0) {  // wall_distance.cpp:54
       precision_of(precision);
@@ -869,6 +876,8 @@ int im_update_volume(im_context* ctx, const double* nodes, size_t n_nodes, const
     const D2HJob down[2] = {{active, entry_nodes, na, 4, true}, {vals, entry_values, 3 * na, 8, false}};
     staged_d2h(c, down, 2);
     *n_entries = na;
+    c.last_h2d_bytes = 32ull * n_nodes + 48ull * nc;
+    c.last_d2h_bytes = 28ull * na;
     tr.mark("d2h");
   });
 }

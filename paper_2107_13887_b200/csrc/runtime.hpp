@@ -125,6 +125,8 @@ struct Context {
   DBuf<unsigned char> scratch;
   HBuf<unsigned char> pinned;
   double last_kernel_ms = 0.0;
+  // host<->device bytes the last im_update_volume actually moved (selective upload)
+  unsigned long long last_h2d_bytes = 0, last_d2h_bytes = 0;
   size_t error_line = 0;  // line of the last IM_PARSE_ERROR
   // Grow-only device scratch slots reused across calls (no cudaMalloc /
   // cudaFree -- which synchronises the device -- on the hot path).
@@ -133,7 +135,7 @@ struct Context {
     kSlotTiles, kSlotBoxes, kSlotStage, kSlotCell, kSlotCounts, kSlotStart, kSlotBox,
     kSlotScanA, kSlotScanB, kSlotElemKind, kSlotElemOffset, kSlotElemNodes, kSlotSortKeyA,
     kSlotSortKeyB, kSlotSortTemp, kSlotIndex, kSlotIndexBox, kSlotBlockOrder, kSlotChunkMax,
-    kSlotScaledTiles, kSlotCount
+    kSlotScaledTiles, kSlotActiveMasks, kSlotWallTree, kSlotCount
   };
   DBuf<unsigned char> slots[kSlotCount];
   std::shared_ptr<HostIOState> io;  // created on first staged transfer

@@ -174,40 +174,55 @@ void wall_distance(Context& ctx, const DPoints& nodes, size_t n_nodes, const DPo
       throw InvalidArgument("surface coordinates are not finite");
   double scale[3];
   for (int a = 0; a < 3; ++a) scale[a] = hi[a] > lo[a] ? 2097151.0 / (hi[a] - lo[a]) : 0.0;
-  // Morton sort of the surface points
-  DBuf<unsigned long long> ka, kb;
-  DBuf<unsigned int> ia, ib;
-  ka.reserve(n_surface), kb.reserve(n_surface), ia.reserve(n_surface), ib.reserve(n_surface);
-  const int T = 256;
-  k_surface_keys<<<(ns + T - 1) / T, T, 0, ctx.stream>>>(surface.x.p, surface.y.p, surface.z.p, ns,
-                                                          lo[0], lo[1], lo[2], scale[0], scale[1],
-                                                          scale[2], ka.p, ia.p);
-  size_t temp = 0;
-  IMB_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, temp, ka.p, kb.p, ia.p, ib.p, ns, 0, 63,
-                                            ctx.stream));
-  DBuf<unsigned char> tb;
-  tb.reserve(temp);
-  IMB_CHECK(cub::DeviceRadixSort::SortPairs(tb.p, temp, ka.p, kb.p, ia.p, ib.p, ns, 0, 63,
-                                            ctx.stream));
-  DBuf<double> sx, sy, sz;
-  sx.reserve(n_surface), sy.reserve(n_surface), sz.reserve(n_surface);
-  k_gather_sorted<<<(ns + T - 1) / T, T, 0, ctx.stream>>>(surface.x.p, surface.y.p, surface.z.p,
-                                                           ib.p, ns, sx.p, sy.p, sz.p);
   // implicit tree: L leaves (power of two >= buckets), boxes in heap order
   int L = 1;
   while ((size_t)L * kLeaf < n_surface) L *= 2;
-  DBuf<double> box;
-  box.reserve((size_t)2 * L * 6);
-  Tree t{L, ns, box.p, sx.p, sy.p, sz.p};
-  k_leaf_boxes<<<(L + T - 1) / T, T, 0, ctx.stream>>>(t, box.p);
+  // every buffer of the build comes out of one grow-only context slot (no
+  // cudaMalloc / cudaFree per call: with tens of GB resident they cost more
+  // than the search itself)
+  size_t temp = 0;
+  IMB_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, temp, (unsigned long long*)nullptr,
+                                            (unsigned long long*)nullptr, (unsigned int*)nullptr,
+                                            (unsigned int*)nullptr, ns, 0, 63, ctx.stream));
+  auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t b_key = up(n_surface * 8), b_idx = up(n_surface * 4), b_pts = up(n_surface * 8),
+               b_box = up((size_t)2 * L * 6 * 8), b_tmp = up(temp);
+  unsigned char* base = ctx.buf<unsigned char>(Context::kSlotWallTree,
+                                               2 * b_key + 2 * b_idx + 3 * b_pts + b_box + b_tmp);
+  unsigned char* cur = base;
+  auto take = [&](size_t b) {
+    unsigned char* r = cur;
+    cur += b;
+    return r;
+  };
+  auto* ka = reinterpret_cast<unsigned long long*>(take(b_key));
+  auto* kb = reinterpret_cast<unsigned long long*>(take(b_key));
+  auto* ia = reinterpret_cast<unsigned int*>(take(b_idx));
+  auto* ib = reinterpret_cast<unsigned int*>(take(b_idx));
+  auto* sx = reinterpret_cast<double*>(take(b_pts));
+  auto* sy = reinterpret_cast<double*>(take(b_pts));
+  auto* sz = reinterpret_cast<double*>(take(b_pts));
+  auto* box = reinterpret_cast<double*>(take(b_box));
+  unsigned char* tbp = take(b_tmp);
+  // Morton sort of the surface points
+  const int T = 256;
+  k_surface_keys<<<(ns + T - 1) / T, T, 0, ctx.stream>>>(surface.x.p, surface.y.p, surface.z.p, ns,
+                                                          lo[0], lo[1], lo[2], scale[0], scale[1],
+                                                          scale[2], ka, ia);
+  IMB_CHECK(cub::DeviceRadixSort::SortPairs(tbp, temp, ka, kb, ia, ib, ns, 0, 63,
+                                            ctx.stream));
+  k_gather_sorted<<<(ns + T - 1) / T, T, 0, ctx.stream>>>(surface.x.p, surface.y.p, surface.z.p,
+                                                           ib, ns, sx, sy, sz);
+  Tree t{L, ns, box, sx, sy, sz};
+  k_leaf_boxes<<<(L + T - 1) / T, T, 0, ctx.stream>>>(t, box);
   for (int first = L / 2; first >= 1; first /= 2)
-    k_inner_boxes<<<(first + T - 1) / T, T, 0, ctx.stream>>>(box.p, first);
+    k_inner_boxes<<<(first + T - 1) / T, T, 0, ctx.stream>>>(box, first);
   IMB_LAUNCH_CHECK();
   const double cutoff2 = std::isfinite(cutoff) ? cutoff * cutoff : INFINITY;
   k_wall_distance<<<(n_nodes + T - 1) / T, T, 0, ctx.stream>>>(t, nodes.x.p, nodes.y.p, nodes.z.p,
                                                                 n_nodes, cutoff2, d_out);
   IMB_LAUNCH_CHECK();
-  IMB_CHECK(cudaStreamSynchronize(ctx.stream));  // local buffers die here
+  IMB_CHECK(cudaStreamSynchronize(ctx.stream));
 }
 
 }  // namespace imb
