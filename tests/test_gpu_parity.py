@@ -217,6 +217,23 @@ def test_update_volume_raw(gpu, oracle, R, D):
     assert np.array_equal(i0, i2) and rel_err(v2, v0) < FAST_TOL
 
 
+@pytest.mark.parametrize("n", [1, 31, 33, 4095, 4097, 100003])
+@pytest.mark.parametrize("D", [0.3, 1e-12, math.inf])
+def test_active_set_ragged_sizes(gpu, oracle, n, D):
+    """The active set (d < D, ascending node ids; wall_distance.cpp:56-58) for
+    mesh sizes around the compaction's 32-node ballots and 4096-node tiles,
+    with none / some / all nodes active."""
+    rng = np.random.default_rng(n)
+    nodes = rng.random((n, 3))
+    d = rng.random(n)
+    d[::7] = 0.0
+    ctrl = rng.random((5, 3))
+    alpha = rng.standard_normal((5, 3))
+    i0, v0 = oracle.update_volume(nodes, d, ctrl, alpha, D, 0, "c2", 0.8)
+    i1, v1 = gpu.update_volume(nodes, d, ctrl, alpha, D, 0, "c2", 0.8, capi.EXACT)
+    assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
+
+
 def test_update_volume_edge_cases(gpu):
     nodes = np.array([[0, 0, 0], [0, 0.05, 0], [0, 0.2, 0], [0, 5, 0]], float)
     d = gpu.build_distance_index(nodes, 2, [0])

@@ -1,7 +1,7 @@
 """The HBM-side passes alone (wall distance K6, compaction K7) on a BASELINE
 mesh: `python tools/hbm_passes.py cfg3 [scale] [cutoff]`.  Used plain for the
 timings and under ncu for the captures in profiles/ (the kernels of interest
-are k_wall_distance, k_count_active, k_scan_counts, k_scatter_active)."""
+are k_wall_distance and k_compact_active)."""
 import json
 import os
 import sys

@@ -28,7 +28,7 @@ ncu --set full --import-source on --clock-control none -k regex:k_volume_exact_t
 ncu -i /tmp/k_exact.ncu-rep --page raw --csv > $A/ncu_k_volume_exact_tiled_cfg4_raw.csv 2>/dev/null
 ncu -i /tmp/k_exact.ncu-rep --page details --csv > $A/ncu_k_volume_exact_tiled_cfg4_details.csv 2>/dev/null
 python tools/hbm_passes.py cfg3 1.0 1.0 1 > $A/hbm_cfg3.json 2>&1 && \
-ncu --set full --clock-control none -k regex:"k_count_active|k_scan_counts|k_scatter_active" -c 6 -o /tmp/cp -f python tools/hbm_passes.py cfg3 1.0 1.0 1 > $A/ncu_cp.log 2>&1
-ncu -i /tmp/cp.ncu-rep --page raw --csv > $A/ncu_compaction_cfg3_raw.csv 2>/dev/null
-ncu -i /tmp/cp.ncu-rep --page details --csv > $A/ncu_compaction_cfg3_details.csv 2>/dev/null
+ncu --set full --clock-control none -k regex:"k_compact_active" -c 3 -o /tmp/cp -f python tools/hbm_passes.py cfg3 1.0 1.0 1 > $A/ncu_cp.log 2>&1
+ncu -i /tmp/cp.ncu-rep --page raw --csv > $A/ncu_k_compact_active_cfg3_raw.csv 2>/dev/null
+ncu -i /tmp/cp.ncu-rep --page details --csv > $A/ncu_k_compact_active_cfg3_details.csv 2>/dev/null
 du -sh gpurun_out; ls -la $A
