@@ -135,7 +135,7 @@ struct Context {
     kSlotTiles, kSlotBoxes, kSlotStage, kSlotCell, kSlotCounts, kSlotStart, kSlotBox,
     kSlotScanA, kSlotScanB, kSlotElemKind, kSlotElemOffset, kSlotElemNodes, kSlotSortKeyA,
     kSlotSortKeyB, kSlotSortTemp, kSlotIndex, kSlotIndexBox, kSlotBlockOrder, kSlotChunkMax,
-    kSlotScaledTiles, kSlotWallTree, kSlotCount
+    kSlotScaledTiles, kSlotWallTree, kSlotWallIds, kSlotWallOrder, kSlotCount
   };
   DBuf<unsigned char> slots[kSlotCount];
   std::shared_ptr<HostIOState> io;  // created on first staged transfer

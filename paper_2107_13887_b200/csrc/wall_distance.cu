@@ -27,6 +27,7 @@
 // scale); the tree visits O(log N_s) boxes.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -107,12 +108,26 @@ __device__ __forceinline__ double box_lb(const double* b, double qx, double qy, 
   return gx * gx + gy * gy + gz * gz;
 }
 
-__global__ void __launch_bounds__(256) k_wall_distance(Tree t, const double* __restrict__ qx_,
-                                                       const double* __restrict__ qy_,
-                                                       const double* __restrict__ qz_, size_t n,
-                                                       double cutoff2, double* out) {
+// every node: lower bound of its distance to the patch's root box against the
+// cutoff -> +inf (out of range, final) or 0 (in range, to be searched)
+__global__ void k_root_test(Tree t, const double* __restrict__ qx, const double* __restrict__ qy,
+                            const double* __restrict__ qz, size_t n, double cutoff2, double* out) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  out[i] = box_lb(t.box + 6, qx[i], qy[i], qz[i]) * (1.0 - 1e-9) > cutoff2 ? INFINITY : 0.0;
+}
+
+// ids / order: the in-range nodes in spatial (Morton) order, or null = all n
+// nodes in mesh order.  Neighbouring lanes then walk nearly the same boxes.
+__global__ void __launch_bounds__(256) k_wall_distance(Tree t, const double* __restrict__ qx_,
+                                                       const double* __restrict__ qy_,
+                                                       const double* __restrict__ qz_,
+                                                       const uint32_t* __restrict__ ids,
+                                                       const uint32_t* __restrict__ order, size_t n,
+                                                       double cutoff2, double* out) {
+  const size_t kk = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (kk >= n) return;
+  const size_t i = ids ? ids[order[kk]] : kk;
   const double qx = qx_[i], qy = qy_[i], qz = qz_[i];
   const double margin = 1.0 - 1e-9;
   double best = INFINITY;
@@ -219,8 +234,28 @@ void wall_distance(Context& ctx, const DPoints& nodes, size_t n_nodes, const DPo
     k_inner_boxes<<<(first + T - 1) / T, T, 0, ctx.stream>>>(box, first);
   IMB_LAUNCH_CHECK();
   const double cutoff2 = std::isfinite(cutoff) ? cutoff * cutoff : INFINITY;
-  k_wall_distance<<<(n_nodes + T - 1) / T, T, 0, ctx.stream>>>(t, nodes.x.p, nodes.y.p, nodes.z.p,
-                                                                n_nodes, cutoff2, d_out);
+  // Queries in mesh order make the lanes of a warp walk different parts of
+  // the tree (far layers of a structured mesh: 32 consecutive nodes span a
+  // wide arc).  So: root test for every node, stable compaction of the
+  // in-range ones, Morton order of those, and the walk in that order.
+  // (measured, sorted vs mesh order: cfg4 mesh 46.7 vs 60.3 ms, cfg3 14.9 vs
+  // 16.1 ms, cfg3 without a cutoff 92 vs 139 ms; below a few million nodes
+  // the extra passes cost more than they save: cfg2 1.13 vs 1.00 ms)
+  if (n_nodes < ((size_t)1 << 22) || std::getenv("IMB_WD_UNSORTED")) {
+    k_wall_distance<<<(n_nodes + T - 1) / T, T, 0, ctx.stream>>>(
+        t, nodes.x.p, nodes.y.p, nodes.z.p, nullptr, nullptr, n_nodes, cutoff2, d_out);
+  } else {
+    k_root_test<<<(n_nodes + T - 1) / T, T, 0, ctx.stream>>>(t, nodes.x.p, nodes.y.p, nodes.z.p,
+                                                              n_nodes, cutoff2, d_out);
+    uint32_t* ids = ctx.buf<uint32_t>(Context::kSlotWallIds, n_nodes);
+    const size_t na = compact_active(ctx, d_out, n_nodes, INFINITY, ids);
+    if (na) {
+      uint32_t* order = ctx.buf<uint32_t>(Context::kSlotWallOrder, na);
+      spatial_order(ctx, nodes.x.p, nodes.y.p, nodes.z.p, ids, na, 1.0, order);
+      k_wall_distance<<<(na + T - 1) / T, T, 0, ctx.stream>>>(t, nodes.x.p, nodes.y.p, nodes.z.p, ids,
+                                                               order, na, cutoff2, d_out);
+    }
+  }
   IMB_LAUNCH_CHECK();
   IMB_CHECK(cudaStreamSynchronize(ctx.stream));
 }
