@@ -70,6 +70,10 @@ def main():
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--threads", type=int, default=max(1, (os.cpu_count() or 2) - 1))
     ap.add_argument("--configs", default="cfg3,cfg4")
+    ap.add_argument("--levels", type=int, default=0,
+                    help="--full: run only the first N levels (0 = the config's count); cfg4's "
+                         "fixture holds levels 0-1 (109 points + one capped level, ~20 min on 7 "
+                         "threads; all four take ~1.5 h)")
     args = ap.parse_args()
     port = Oracle("port")
     port.set_sweep_threads(args.threads)
@@ -93,6 +97,8 @@ def main():
     out = dict(np.load(path)) if os.path.exists(path) else {}
     for name in args.configs.split(","):
         pos, disp, R, tol, levels = W.wing_surface_case(name)
+        if args.levels:
+            levels = min(levels, args.levels)
         t0 = time.time()
         try:
             m = port.run_multilevel(pos, disp, tol, levels, 5000, "c2", R)
