@@ -308,6 +308,15 @@ def run_b200(args):
         torch.distributed.barrier()
     value = world * pairs_step / (step_ms * 1e-3) / 1e9
 
+    # pairs the exact kernels actually evaluate (tile / warp-box culling leaves
+    # more than the pairs in support): one extra, untimed step with the
+    # library's pair counter on
+    pairs_evaluated = None
+    if prec == capi.EXACT:
+        ctx.count_pairs(True)
+        plan.run_steps(1, "c2", R, prec, flush_l2=False)
+        pairs_evaluated = ctx.count_pairs(False)
+
     # roofline of the dominant kernel (the volume update): algorithmic flops
     # per launch / average launch time (CUDA events on the context stream)
     # Only in-support pairs are counted: the kernel skips out-of-support pairs
@@ -333,6 +342,9 @@ def run_b200(args):
                 if prec == capi.EXACT
                 else 0 if prec == capi.FP32 else (16 if dim == 3 else 14)}
     if prec == capi.EXACT:
+        if pairs_evaluated:
+            roofline["pairs_evaluated_per_step"] = int(pairs_evaluated)
+            roofline["evaluated_per_in_support"] = round(pairs_evaluated / max(in_step, 1), 3)
         roofline["exact_division"] = exact_division_form(R)
         roofline["instruction_cap_frac"] = round(fin / (2.0 * roofline["fp64_instructions_per_pair"]), 4)
     if prec == capi.FP32:

@@ -93,6 +93,11 @@ double im_last_device_ms(const im_context* ctx);
  * selective upload skips node chunks without active nodes); measurement aid */
 void im_last_transfer_bytes(const im_context* ctx, unsigned long long* h2d,
                             unsigned long long* d2h);
+/* diagnostic: switches the exact volume kernels' pair counter on / off and
+ * returns the pairs they evaluated since the previous call (culling leaves
+ * more pairs evaluated than are in support; the counter slows the kernels and
+ * is never on inside a timed region) */
+unsigned long long im_count_pairs(im_context* ctx, int enable);
 /* library build tag (sm_100a) */
 const char* im_version(void);
 

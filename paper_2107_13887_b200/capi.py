@@ -105,7 +105,7 @@ def load_library() -> C.CDLL:
 
 EXPORTS = [
     "im_context_create", "im_context_destroy", "im_last_error", "im_last_device_ms",
-    "im_last_transfer_bytes",
+    "im_last_transfer_bytes", "im_count_pairs",
     "im_version", "im_eval_wendland", "im_eval_basis", "im_make_wall_function",
     "im_eval_wall_function", "im_solve_weights", "im_eval_interpolant", "im_greedy_level",
     "im_run_multilevel", "im_build_distance_index", "im_signed_measures", "im_count_inverted", "im_orthogonality",
@@ -130,6 +130,8 @@ def _declare(L):
     L.im_last_transfer_bytes.argtypes = [C.c_void_p, C.POINTER(C.c_ulonglong),
                                          C.POINTER(C.c_ulonglong)]
     L.im_last_transfer_bytes.restype = None
+    L.im_count_pairs.argtypes = [C.c_void_p, C.c_int]
+    L.im_count_pairs.restype = C.c_ulonglong
     L.im_version.restype = C.c_char_p
     L.im_eval_wendland.argtypes = [C.c_int, _d]
     L.im_eval_wendland.restype = _d
@@ -288,6 +290,11 @@ class Context:
         a, b = C.c_ulonglong(), C.c_ulonglong()
         self.lib.im_last_transfer_bytes(self.h, C.byref(a), C.byref(b))
         return a.value, b.value
+
+    def count_pairs(self, enable: bool) -> int:
+        """Switch the exact kernels' evaluated-pair counter; returns the count
+        accumulated since the previous call."""
+        return int(self.lib.im_count_pairs(self.h, 1 if enable else 0))
 
     # -- rbf ---------------------------------------------------------------
     def solve_weights(self, points, displacements, kind="c2", R=1.0) -> np.ndarray:

@@ -248,6 +248,13 @@ int im_context_destroy(im_context* ctx) {
 
 const char* im_last_error(const im_context* ctx) { return ctx ? ctx->c.message : "null context"; }
 double im_last_device_ms(const im_context* ctx) { return ctx ? ctx->c.last_kernel_ms : 0.0; }
+unsigned long long im_count_pairs(im_context* ctx, int enable) {
+  if (!ctx) return 0;
+  const unsigned long long n = ctx->c.pairs_evaluated;
+  ctx->c.count_pairs = enable != 0;
+  ctx->c.pairs_evaluated = 0;
+  return n;
+}
 void im_last_transfer_bytes(const im_context* ctx, unsigned long long* h2d, unsigned long long* d2h) {
   if (h2d) *h2d = ctx ? ctx->c.last_h2d_bytes : 0;
   if (d2h) *d2h = ctx ? ctx->c.last_d2h_bytes : 0;

@@ -722,7 +722,7 @@ int im_volume_plan_run_steps(im_volume_plan* p, im_basis basis, int precision, i
         size_t na = last_na;
         if (!(L.D == last_D)) {
           na = compact_active(c, p->dist.p, p->n, L.D, p->active.p);
-          per_step += 3;
+          per_step += 1;  // k_compact_active
           last_D = L.D, last_na = na;
         }
         if (l < 4) stats[4 + l] = (double)na;

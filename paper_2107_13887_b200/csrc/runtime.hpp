@@ -127,6 +127,9 @@ struct Context {
   double last_kernel_ms = 0.0;
   // host<->device bytes the last im_update_volume actually moved (selective upload)
   unsigned long long last_h2d_bytes = 0, last_d2h_bytes = 0;
+  // diagnostic (im_count_pairs): the exact kernels count the pairs they evaluate
+  bool count_pairs = false;
+  unsigned long long pairs_evaluated = 0;
   size_t error_line = 0;  // line of the last IM_PARSE_ERROR
   // Grow-only device scratch slots reused across calls (no cudaMalloc /
   // cudaFree -- which synchronises the device -- on the hot path).
